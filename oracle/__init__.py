@@ -1,0 +1,18 @@
+"""fp64 CPU oracle for the fused attention forward — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package. The product path
+(``paper_2504_17577_b200``) never imports it and shares no code with it.
+See ``oracle/oracle.h`` for the definition and its citations (PAPER.md P:L424,
+P:L583, Fig. 18).
+"""
+from .oracle import (  # noqa: F401
+    build_oracle,
+    widen,
+    attn_rows,
+    attn_rows_parallel,
+    attn_full,
+    brute_force,
+    ORACLE_F16,
+    ORACLE_BF16,
+)

@@ -1,0 +1,61 @@
+/*
+ * oracle.h — fp64 CPU oracle for the fused attention forward.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (libtlattn) never links, loads or calls it, and the two share no code.
+ *
+ * What it computes (ref [12] "exact attention"; the recurrence of
+ * Fig. 18, is an exact reformulation of the same result):
+ *
+ *   o[b,i,h,:] = sum_{j in J_i} softmax_j(scale * q[b,i,h,:].k[b,j,g,:]) * v[b,j,g,:]
+ *   g   = h / (Hq / Hkv)                        (GQA grouping; R7)
+ *   J_i = { j < Skv : !causal || j <= i + Skv - Sq }   (bottom-right causal, R3)
+ *   lse[b,h,i] = log sum_{j in J_i} exp(scale * q.k_j)  (natural log, R5)
+ *   J_i empty -> o = 0, lse = -inf                       (R4)
+ *
+ * Layout (R6): q[B][Sq][Hq][D], k,v[B][Skv][Hkv][D] as raw 16-bit patterns
+ * (dtype 0 = IEEE fp16, 1 = bfloat16), widened exactly to double.
+ *
+ * Return codes: 0 ok, 1 invalid argument (nothing written).
+ */
+#ifndef TLATTN_ORACLE_H
+#define TLATTN_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORACLE_F16 = 0, ORACLE_BF16 = 1 };
+
+/* Exact widening of one 16-bit pattern to double (IEEE binary16 / bfloat16). */
+double oracle_widen(uint16_t bits, int dtype);
+
+/* Plain-definition attention for selected query rows of one (b, h).
+ * rows[nrows] are query indices in [0, Sq). o_out is nrows x D (row-major),
+ * lse_out is nrows (may be NULL). Two-pass form: max, then exp/sum/normalise. */
+int oracle_attn_rows(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                     long B, long Hq, long Hkv, long Sq, long Skv, long D,
+                     int causal, double scale, long b, long h,
+                     const long* rows, long nrows, double* o_out, double* lse_out);
+
+/* All rows of all (b, h): o_out is BSHD [B][Sq][Hq][D], lse_out is [B][Hq][Sq]. */
+int oracle_attn_full(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                     long B, long Hq, long Hkv, long Sq, long Skv, long D,
+                     int causal, double scale, double* o_out, double* lse_out);
+
+/* Independent brute-force formulation for tiny shapes (one (b, h)):
+ * materialises S (Sq x Skv, -inf where masked), P_ij = 1 / sum_k exp(s_ik - s_ij)
+ * (no max subtraction), O = P V as an explicit matrix product.
+ * s_out/p_out (Sq x Skv) may be NULL; o_out is Sq x D; lse_out is Sq (may be NULL). */
+int oracle_brute_force(const uint16_t* q, const uint16_t* k, const uint16_t* v, int dtype,
+                       long B, long Hq, long Hkv, long Sq, long Skv, long D,
+                       int causal, double scale, long b, long h,
+                       double* s_out, double* p_out, double* o_out, double* lse_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,141 @@
+"""ctypes loader for liboracle.so (plain C, fp64) — TEST INFRASTRUCTURE ONLY.
+
+Inputs are numpy ``uint16`` arrays holding the raw fp16/bf16 bit patterns of
+contiguous BSHD tensors (R6). Outputs are float64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ORACLE_F16 = 0
+ORACLE_BF16 = 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = [os.path.join(_HERE, "attn_oracle.c")]
+_lock = threading.Lock()
+_lib = None
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile liboracle.so with gcc -O2 (no -ffast-math). Returns the path."""
+    newest_src = max(os.path.getmtime(p) for p in _SRC + [os.path.join(_HERE, "oracle.h")])
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest_src:
+        tmp = _SO + f".tmp{os.getpid()}"
+        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-Wextra",
+               "-o", tmp, *_SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build_oracle())
+            L, I, D = ctypes.c_long, ctypes.c_int, ctypes.c_double
+            P16 = ctypes.POINTER(ctypes.c_uint16)
+            PD = ctypes.POINTER(ctypes.c_double)
+            PL = ctypes.POINTER(ctypes.c_long)
+            lib.oracle_widen.argtypes = [ctypes.c_uint16, I]
+            lib.oracle_widen.restype = D
+            lib.oracle_attn_rows.argtypes = [P16, P16, P16, I, L, L, L, L, L, L, I, D, L, L,
+                                             PL, L, PD, PD]
+            lib.oracle_attn_rows.restype = I
+            lib.oracle_attn_full.argtypes = [P16, P16, P16, I, L, L, L, L, L, L, I, D, PD, PD]
+            lib.oracle_attn_full.restype = I
+            lib.oracle_brute_force.argtypes = [P16, P16, P16, I, L, L, L, L, L, L, I, D, L, L,
+                                               PD, PD, PD, PD]
+            lib.oracle_brute_force.restype = I
+            _lib = lib
+    return _lib
+
+
+def _p16(a: np.ndarray):
+    assert a.dtype == np.uint16 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16))
+
+
+def _pd(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _dims(q, k, v):
+    assert q.ndim == 4 and k.ndim == 4 and v.ndim == 4 and k.shape == v.shape
+    B, Sq, Hq, D = q.shape
+    Bk, Skv, Hkv, Dk = k.shape
+    assert Bk == B and Dk == D
+    return B, Hq, Hkv, Sq, Skv, D
+
+
+def widen(bits: int, dtype: int) -> float:
+    return _load().oracle_widen(ctypes.c_uint16(bits), dtype)
+
+
+def attn_rows(q, k, v, dtype, causal, scale, b, h, rows):
+    """Oracle output for query rows ``rows`` of head (b, h): (o[nrows, D], lse[nrows])."""
+    lib = _load()
+    B, Hq, Hkv, Sq, Skv, D = _dims(q, k, v)
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    n = rows.shape[0]
+    o = np.zeros((n, D), np.float64)
+    lse = np.zeros((n,), np.float64)
+    rc = lib.oracle_attn_rows(_p16(q), _p16(k), _p16(v), dtype, B, Hq, Hkv, Sq, Skv, D,
+                              int(causal), float(scale), int(b), int(h),
+                              rows.ctypes.data_as(ctypes.POINTER(ctypes.c_long)), n,
+                              _pd(o), _pd(lse))
+    if rc != 0:
+        raise ValueError(f"oracle_attn_rows rejected its arguments (rc={rc})")
+    return o, lse
+
+
+def attn_rows_parallel(q, k, v, dtype, causal, scale, work, threads=None):
+    """Run ``attn_rows`` over independent (b, h, rows) items on host threads.
+
+    ``work`` is a list of (b, h, rows). Each call is single-threaded C (ctypes drops
+    the GIL), so the items run concurrently. Returns a list of (o, lse).
+    """
+    threads = threads or len(os.sched_getaffinity(0))
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        futs = [ex.submit(attn_rows, q, k, v, dtype, causal, scale, b, h, rows)
+                for (b, h, rows) in work]
+        return [f.result() for f in futs]
+
+
+def attn_full(q, k, v, dtype, causal, scale):
+    """All rows: (o[B,Sq,Hq,D], lse[B,Hq,Sq]) in float64."""
+    lib = _load()
+    B, Hq, Hkv, Sq, Skv, D = _dims(q, k, v)
+    o = np.zeros((B, Sq, Hq, D), np.float64)
+    lse = np.zeros((B, Hq, Sq), np.float64)
+    rc = lib.oracle_attn_full(_p16(q), _p16(k), _p16(v), dtype, B, Hq, Hkv, Sq, Skv, D,
+                              int(causal), float(scale), _pd(o), _pd(lse))
+    if rc != 0:
+        raise ValueError(f"oracle_attn_full rejected its arguments (rc={rc})")
+    return o, lse
+
+
+def brute_force(q, k, v, dtype, causal, scale, b, h):
+    """Explicit-matrix formulation for one (b, h): returns (S, P, O, lse)."""
+    lib = _load()
+    B, Hq, Hkv, Sq, Skv, D = _dims(q, k, v)
+    S = np.zeros((Sq, Skv), np.float64)
+    P = np.zeros((Sq, Skv), np.float64)
+    O = np.zeros((Sq, D), np.float64)
+    lse = np.zeros((Sq,), np.float64)
+    rc = lib.oracle_brute_force(_p16(q), _p16(k), _p16(v), dtype, B, Hq, Hkv, Sq, Skv, D,
+                                int(causal), float(scale), int(b), int(h),
+                                _pd(S), _pd(P), _pd(O), _pd(lse))
+    if rc != 0:
+        raise ValueError(f"oracle_brute_force rejected its arguments (rc={rc})")
+    return S, P, O, lse

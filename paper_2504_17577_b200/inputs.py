@@ -1,0 +1,116 @@
+"""Seeded synthetic inputs shared by the tests, the bench and the oracle checks.
+
+This module holds NO attention arithmetic: it only draws Q/K/V values. It is the one
+module both the CUDA path's callers and the oracle's callers use (DESIGN.md "Input
+recipe", reading R11).
+
+Recipe: Q, K, V iid N(0, 1) rounded round-to-nearest-even to the config dtype,
+contiguous BSHD. Each element is a pure function of (seed, tensor id, global BSHD
+linear index) — a counter-based generator — so a shard of a tensor (a batch or head
+slice) is bit-identical to the same slice of the unsharded tensor.
+
+Generator: u32 = lowbias32(counter ^ key) (two rounds), uniforms from the top 24 bits,
+Box-Muller in fp32. Integer hashing is done in int64 torch ops masked to 32 bits so
+it runs identically on CPU and CUDA tensors.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+TENSOR_ID = {"q": 1, "k": 2, "v": 3}
+_M32 = 0xFFFFFFFF
+
+
+def _lowbias32(x: torch.Tensor) -> torch.Tensor:
+    # x holds values in [0, 2^32) as int64; products wrap mod 2^64 and are masked to 32 bits
+    x = x ^ (x >> 16)
+    x = (x * 0x7FEB352D) & _M32
+    x = x ^ (x >> 15)
+    x = (x * 0x846CA68B) & _M32
+    x = x ^ (x >> 16)
+    return x
+
+
+def _key(seed: int, tensor_id: int) -> int:
+    h = (seed * 0x9E3779B1 + tensor_id * 0x85EBCA77 + 0x165667B1) & _M32
+    # scramble on the host with the same hash
+    return int(_lowbias32(torch.tensor([h], dtype=torch.int64)).item())
+
+
+def normal_from_index(idx: torch.Tensor, seed: int, tensor_id: int) -> torch.Tensor:
+    """N(0,1) fp32 values for int64 global indices ``idx`` (any device)."""
+    key = _key(seed, tensor_id)
+    c0 = (idx * 2) & _M32
+    c1 = (idx * 2 + 1) & _M32
+    hi = (idx >> 31) & _M32  # extra counter bits for tensors with > 2^31 elements
+    h0 = _lowbias32(_lowbias32(c0 ^ key) ^ hi)
+    h1 = _lowbias32(_lowbias32(c1 ^ key) ^ hi)
+    u1 = ((h0 >> 8).to(torch.float32) + 0.5) * (1.0 / 16777216.0)
+    u2 = ((h1 >> 8).to(torch.float32) + 0.5) * (1.0 / 16777216.0)
+    r = torch.sqrt(-2.0 * torch.log(u1))
+    return r * torch.cos((2.0 * math.pi) * u2)
+
+
+def gen_tensor(shape, seed: int, name: str, dtype: torch.dtype, device,
+               slices=None, chunk: int = 1 << 25) -> torch.Tensor:
+    """Contiguous tensor of ``shape`` (global BSHD shape), optionally a sub-block.
+
+    ``slices`` is a tuple of python ``slice`` objects over the global shape (step 1);
+    the result holds exactly those elements of the global tensor.
+    """
+    shape = tuple(int(s) for s in shape)
+    if slices is None:
+        slices = tuple(slice(0, s) for s in shape)
+    ranges = [range(*sl.indices(s)) for sl, s in zip(slices, shape)]
+    out_shape = tuple(len(r) for r in ranges)
+    out = torch.empty(out_shape, dtype=dtype, device=device)
+    n = out.numel()
+    if n == 0:
+        return out
+    strides = [1] * len(shape)
+    for i in range(len(shape) - 2, -1, -1):
+        strides[i] = strides[i + 1] * shape[i + 1]
+    flat = out.view(-1)
+    # Enumerate local linear indices in chunks and map them to global linear indices.
+    out_strides = [1] * len(out_shape)
+    for i in range(len(out_shape) - 2, -1, -1):
+        out_strides[i] = out_strides[i + 1] * out_shape[i + 1]
+    tid = TENSOR_ID[name]
+    for start in range(0, n, chunk):
+        stop = min(n, start + chunk)
+        loc = torch.arange(start, stop, dtype=torch.int64, device=device)
+        gidx = torch.zeros_like(loc)
+        rem = loc
+        for dim in range(len(out_shape)):
+            coord = rem // out_strides[dim]
+            rem = rem - coord * out_strides[dim]
+            gidx += (coord + ranges[dim].start) * strides[dim]
+        flat[start:stop] = normal_from_index(gidx, seed, tid).to(dtype)
+    return out
+
+
+def gen_qkv(B, Hq, Hkv, Sq, Skv, D, dtype, seed, device, b_slice=None, hq_slice=None,
+            hkv_slice=None):
+    """Q[B,Sq,Hq,D], K/V[B,Skv,Hkv,D] (or the given batch/head shard of them)."""
+    bs = b_slice or slice(0, B)
+    q = gen_tensor((B, Sq, Hq, D), seed, "q", dtype, device,
+                   (bs, slice(0, Sq), hq_slice or slice(0, Hq), slice(0, D)))
+    k = gen_tensor((B, Skv, Hkv, D), seed, "k", dtype, device,
+                   (bs, slice(0, Skv), hkv_slice or slice(0, Hkv), slice(0, D)))
+    v = gen_tensor((B, Skv, Hkv, D), seed, "v", dtype, device,
+                   (bs, slice(0, Skv), hkv_slice or slice(0, Hkv), slice(0, D)))
+    return q, k, v
+
+
+def to_bits(t: torch.Tensor) -> np.ndarray:
+    """Raw 16-bit patterns of an fp16/bf16 tensor as a host numpy uint16 array."""
+    assert t.dtype in (torch.float16, torch.bfloat16)
+    return t.detach().contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def from_values(values, dtype: torch.dtype, device="cpu") -> torch.Tensor:
+    """Tensor of the given (float) values rounded RN to ``dtype``."""
+    return torch.as_tensor(np.asarray(values, dtype=np.float32)).to(dtype).to(device)
