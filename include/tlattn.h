@@ -1,0 +1,115 @@
+/*
+ * tlattn.h — C ABI of libtlattn, the B200 (sm_100a) fused attention forward.
+ *
+ * Operation (§5.2 P:L362 / Fig. 12: the FlashAttention forward; Fig. 18
+ * P:L573-696 gives the tiled online-softmax algorithm; "exact attention", ref [12]
+ * P:L424):
+ *
+ *   o[b,i,h,:] = sum_{j in J_i} softmax_j( scale * q[b,i,h,:] . k[b,j,g,:] ) * v[b,j,g,:]
+ *   g   = h / (Hq / Hkv)                 GQA grouping, cur_kv_head
+ *   J_i = { 0 <= j < Skv : !causal || j <= i + Skv - Sq }   (bottom-right causal)
+ *   lse[b,h,i] = ln sum_{j in J_i} exp(scale * q.k_j)        (natural log)
+ *   J_i empty (only causal with Sq > Skv): o = 0, lse = -inf
+ *
+ * Precision (P:L592, P:L602-614 dtype / accum_dtype): q, k, v, o are fp16 or bf16;
+ * S = QK^T and O = PV accumulate in fp32 (tensor-core TMEM accumulators); the
+ * running max and row sum are fp32, the row sum is taken over the unrounded fp32
+ * probabilities; P is rounded to the input dtype (round-to-nearest-even) before
+ * the PV product; O is rounded RN on output.
+ *
+ * Layout (KV[batch, seqlen_kv, kv_head_num, dim]): contiguous BSHD,
+ *   q[B][Sq][Hq][D], k[B][Skv][Hkv][D], v[B][Skv][Hkv][D], o[B][Sq][Hq][D],
+ *   lse[B][Hq][Sq] fp32.
+ *
+ * Ownership: the caller owns every buffer. The library allocates no device memory
+ * and keeps no pointer after a call returns; it caches only immutable per-device
+ * attributes (SM count, compute capability), initialised thread-safely.
+ * o / lse must not alias q / k / v.
+ *
+ * Synchronisation: tl_attn_fwd is stream-ordered and asynchronous (no host sync, no
+ * allocation: CUDA-graph capturable). Device faults surface at the caller's next
+ * synchronisation, as usual for CUDA.
+ *
+ * Errors: argument errors are returned synchronously BEFORE any CUDA call and
+ * nothing is launched. There is no CPU fallback: a device that is not sm_100
+ * returns TL_ERR_UNSUPPORTED.
+ */
+#ifndef TLATTN_H
+#define TLATTN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLATTN_VERSION 0x000100 /* 0.1.0 */
+
+enum tl_dtype { TL_DTYPE_F16 = 0, TL_DTYPE_BF16 = 1 };
+
+enum tl_status {
+  TL_OK = 0,
+  /* NULL q/k/v/o; B, Hq, Hkv, Sq, Skv or D < 1; causal not 0/1; scale not finite;
+     unknown dtype; nbytes/workspace too small (tl_attn_fwd_host) */
+  TL_ERR_INVALID_VALUE = 1,
+  /* D not in {64, 128}; Hq % Hkv != 0; q/k/v/o not 16-byte aligned or lse not 4-byte
+     aligned; a tensor too large for 32-bit TMA coordinates; device not sm_100 */
+  TL_ERR_UNSUPPORTED = 2,
+  /* a CUDA runtime / driver call failed (no device, tensor-map encode, launch) */
+  TL_ERR_CUDA = 3
+};
+
+/*
+ * tl_attn_fwd — fused attention forward on the current CUDA device.
+ *
+ *   q, k, v  device pointers, contiguous BSHD (see above), 16-byte aligned
+ *   o        device pointer, contiguous BSHD [B][Sq][Hq][D], written in full
+ *   lse      device pointer to fp32 [B][Hq][Sq], 4-byte aligned, or NULL (not written)
+ *   B, Hq, Hkv, Sq, Skv, D    sizes; Hq % Hkv == 0; D in {64, 128}; all >= 1
+ *   causal   0 = full attention, 1 = bottom-right causal mask (j <= i + Skv - Sq)
+ *   scale    natural-exp score scale, used literally (callers normally pass 1/sqrt(D));
+ *            0 and negative values are legal
+ *   dtype    TL_DTYPE_F16 or TL_DTYPE_BF16 (q, k, v and o share it)
+ *   stream   cudaStream_t (as void*) to launch on; NULL = legacy default stream
+ *
+ * Returns TL_OK or a tl_status code (see tl_attn_strerror).
+ */
+int tl_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                int causal, float scale, int dtype, void* stream);
+
+/*
+ * tl_attn_fwd_host — the same operation on HOST buffers (the end-to-end entry point).
+ *
+ * q_h, k_h, v_h, o_h, lse_h are host pointers (pinned memory gives full PCIe speed;
+ * lse_h may be NULL). The library stages them through the caller-provided DEVICE
+ * workspace `ws` of `ws_bytes` bytes (>= tl_attn_host_workspace_bytes(...)),
+ * copying inputs host->device, running tl_attn_fwd and copying o (and lse)
+ * device->host on `stream`. Batches are processed in chunks so that the copies of
+ * one chunk overlap the attention of another (two internal chunk slots in `ws`).
+ * Stream-ordered; the host buffers must stay valid until the stream reaches this
+ * point. Returns TL_OK or a tl_status code.
+ */
+int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_h, void* o_h, float* lse_h,
+                     int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                     int causal, float scale, int dtype,
+                     void* ws, uint64_t ws_bytes, void* stream);
+
+/* Device workspace bytes tl_attn_fwd_host needs for this problem (0 on bad arguments). */
+uint64_t tl_attn_host_workspace_bytes(int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                                      int with_lse);
+
+/* Static, NUL-terminated description of a tl_status code. Never NULL. */
+const char* tl_attn_strerror(int status);
+
+/* TLATTN_VERSION of the loaded library. */
+int tl_attn_version(void);
+
+/* Number of kernel launches the most recent successful tl_attn_fwd / tl_attn_fwd_host
+ * call on this host thread issued (tl_attn_fwd: 1). For accounting in benchmarks. */
+int tl_attn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLATTN_H */

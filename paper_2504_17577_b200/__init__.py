@@ -1,0 +1,25 @@
+"""B200-native fused attention forward (the hot path of arXiv 2504.17577, TileLang §5.2).
+
+The product is the C-ABI library ``libtlattn.so`` (include/tlattn.h) built from
+``csrc/``; this package is its thin Python binding plus test/bench plumbing
+(seeded input generator, configs, multi-GPU sharding helpers).
+"""
+from .tlattn import (  # noqa: F401
+    TL_DTYPE_BF16,
+    TL_DTYPE_F16,
+    TL_ERR_CUDA,
+    TL_ERR_INVALID_VALUE,
+    TL_ERR_UNSUPPORTED,
+    TL_OK,
+    HostAttention,
+    TlAttnError,
+    attention,
+    dtype_code,
+    load_library,
+    tl_attn_fwd,
+    tl_attn_fwd_host,
+    tl_attn_host_workspace_bytes,
+    tl_attn_last_launch_count,
+    tl_attn_strerror,
+    tl_attn_version,
+)

@@ -1,0 +1,403 @@
+// attn_fwd_sm100.cuh — fused attention forward for B200 (sm_100a).
+//
+// What it computes: see include/tlattn.h (§5.2; Fig. 18).
+// How (B200-native re-design of the Fig. 18 schedule):
+//
+//   CTA = one "unit" = 2 query tiles of BM=128 rows of one (b, h)   [Fig. 18 tiles
+//         Q_shared / acc_s / acc_o; here M=128 per tcgen05 tile]
+//   warp 0        TMA producer: Q tiles once (T.copy Q), then K_j, V_j into an
+//                 NST-slot mbarrier ring (T.Pipelined num_stages)
+//   warp 1        MMA issuer (one thread): S_t = Q_t K_j^T (T.gemm transpose_B)
+//                 and O_t += P_t V_j (T.gemm) with tcgen05.mma, accumulators
+//                 in TMEM; tcgen05.commit -> mbarriers
+//   warps 4-7     softmax for tile 0, warps 8-11 softmax for tile 1: tcgen05.ld of the
+//                 S row (one thread owns one row: TMEM lane = row), mask, running max,
+//                 exp2, row sum, O rescale in TMEM, P -> smem
+//                 (128B-swizzled, RN to dtype), epilogue O/l and LSE
+//
+// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D)
+// SMEM: Q0,Q1 (2 x 128 x D x 2B) | KV ring NST x (128 x D x 2B) | P0,P1 (2 x 32 KB) | mbarriers
+// All operand tiles are TMA SWIZZLE_128B boxes of 128 rows x 64 elements (16 KB).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace tlattn {
+
+constexpr int BM = 128;            // query rows per tile (tcgen05 M)
+constexpr int BN = 128;            // keys per K/V block (tcgen05 N of QK^T, K of PV)
+constexpr int TILES = 2;           // query tiles per CTA unit
+constexpr int NUM_THREADS = 384;   // 12 warps
+constexpr int SOFTMAX_WARP0 = 4;   // warps 4..11
+constexpr int CHUNK_BYTES = 128 * 128;  // one 128-row x 64-element 16-bit SW128 box
+constexpr uint32_t TMEM_COLS = 512;
+
+struct AttnParams {
+  CUtensorMap tm_q;  // BSHD as 4-D (D, Hq, Sq, B), box (64, 1, 128, 1), SWIZZLE_128B
+  CUtensorMap tm_k;  // (D, Hkv, Skv, B)
+  CUtensorMap tm_v;
+  void* o;           // BSHD output
+  float* lse;        // [B][Hq][Sq] or nullptr
+  int B, Hq, Hkv, Sq, Skv;
+  int causal;
+  float c_log2;      // |scale| * log2(e)
+  int neg;           // scale < 0: negate A (= Q) in the QK^T instruction descriptor
+  int n_mblk;        // ceil(Sq / 256)
+  int n_units;       // B * Hq * n_mblk
+};
+
+template <int D>
+struct KCfg {
+  static constexpr int Q_TILE_BYTES = BM * D * 2;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int NST = (D == 128) ? 3 : 6;
+  static constexpr int P_TILE_BYTES = BM * BN * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = OFF_Q + TILES * Q_TILE_BYTES;
+  static constexpr int OFF_P = OFF_KV + NST * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_P + TILES * P_TILE_BYTES;
+  // barriers: q_full, kv_full[NST], kv_empty[NST], s_full[2], s_free[2], p_full[2], o_done[2]
+  static constexpr int NUM_BARS = 1 + 2 * NST + 8;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_USED = OFF_TMEMPTR + 16;
+  static constexpr int SMEM_BYTES = SMEM_USED + 1024;  // slack for 1024-B alignment
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+  static constexpr uint32_t TMEM_O = 2 * BN;  // O0 column base
+};
+
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t r;
+  if constexpr (BF16) {
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  } else {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  }
+  return r;
+}
+
+// Number of K/V blocks tile starting at row r0 must visit (causal tile skipping).
+__device__ __forceinline__ int tile_nblocks(int r0, const AttnParams& p) {
+  if (r0 >= p.Sq) return 0;
+  const int n_all = (p.Skv + BN - 1) / BN;
+  if (!p.causal) return n_all;
+  const int r_last = min(r0 + BM - 1, p.Sq - 1);
+  const long long kmax = (long long)r_last + p.Skv - p.Sq;  // last key the last row may see
+  if (kmax < 0) return 0;
+  return min(n_all, (int)(kmax / BN) + 1);
+}
+
+template <int D, bool BF16>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
+  using C = KCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B aligned base (SWIZZLE_128B atoms)
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_u32);
+
+  const uint32_t sQ = base + C::OFF_Q;
+  const uint32_t sKV = base + C::OFF_KV;
+  const uint32_t sP = base + C::OFF_P;
+  const uint32_t bar0 = base + C::OFF_BAR;
+  const uint32_t bar_q_full = bar0;
+  auto bar_kv_full = [&](int s) { return bar0 + 8u * (1 + s); };
+  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (1 + C::NST + s); };
+  auto bar_s_full = [&](int t) { return bar0 + 8u * (1 + 2 * C::NST + t); };
+  auto bar_s_free = [&](int t) { return bar0 + 8u * (3 + 2 * C::NST + t); };
+  auto bar_p_full = [&](int t) { return bar0 + 8u * (5 + 2 * C::NST + t); };
+  auto bar_o_done = [&](int t) { return bar0 + 8u * (7 + 2 * C::NST + t); };
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- unit decode: (b, h) major, query block minor; causal: heaviest block first
+  const int u = blockIdx.x;
+  const int mb_i = u % p.n_mblk;
+  const int bh = u / p.n_mblk;
+  const int h = bh % p.Hq;
+  const int b = bh / p.Hq;
+  const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
+  const int hkv = h / (p.Hq / p.Hkv);  // GQA grouping
+  int n_t[TILES];
+#pragma unroll
+  for (int t = 0; t < TILES; ++t) n_t[t] = tile_nblocks(m_blk * (TILES * BM) + t * BM, p);
+  const int nmax = max(n_t[0], n_t[1]);
+
+  // ---- setup
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_q);
+    prefetch_tmap(&p.tm_k);
+    prefetch_tmap(&p.tm_v);
+    mbar_init(bar_q_full, 1);
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(bar_kv_full(s), 1);
+      mbar_init(bar_kv_empty(s), 1);
+    }
+    for (int t = 0; t < TILES; ++t) {
+      mbar_init(bar_s_full(t), 1);
+      mbar_init(bar_s_free(t), 4);
+      mbar_init(bar_p_full(t), 4);
+      mbar_init(bar_o_done(t), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_ptr_smem));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_smem;
+
+  if (warp == 0) {
+    // =========================== TMA producer ===========================
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      uint32_t qbytes = 0;
+#pragma unroll
+      for (int t = 0; t < TILES; ++t)
+        if (m_blk * (TILES * BM) + t * BM < p.Sq) qbytes += C::Q_TILE_BYTES;
+      mbar_arrive_expect_tx(bar_q_full, qbytes);
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        const int r0 = m_blk * (TILES * BM) + t * BM;
+        if (r0 < p.Sq) {
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_4d(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, bar_q_full, c * 64,
+                        h, r0, b, pol_q);
+        }
+      }
+      int it = 0;
+      for (int j = 0; j < nmax; ++j) {
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv, ++it) {
+          const int slot = it % C::NST;
+          const int use = it / C::NST;
+          if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
+          mbar_arrive_expect_tx(bar_kv_full(slot), C::KV_BYTES);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_4d(sKV + slot * C::KV_BYTES + c * CHUNK_BYTES, kv == 0 ? &p.tm_k : &p.tm_v,
+                        bar_kv_full(slot), c * 64, hkv, j * BN, b, pol_kv);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // =========================== MMA issuer ===========================
+    if (lane == 0 && nmax > 0) {
+      constexpr uint32_t FMT = BF16 ? 1u : 0u;
+      // S = Q K^T: A = Q (K-major), B = K (K-major), M=128, N=128
+      const uint32_t IDESC_QK = make_idesc_f16(FMT, BM, BN, 0, 0, p.neg ? 1u : 0u);
+      // O += P V: A = P (K-major), B = V (MN-major: D contiguous), M=128, N=D
+      constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, BM, D, 0, 1, 0);
+      mbar_wait(bar_q_full, 0);
+      tc_fence_after();
+      int it = 0;
+      int v_slot_prev = 0, v_use_prev = 0;
+      auto issue_pv = [&](int jj, int vslot, int vuse) {
+        mbar_wait(bar_kv_full(vslot), vuse & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) {
+          if (jj < n_t[t]) {
+            mbar_wait(bar_p_full(t), jj & 1);
+            tc_fence_after();
+            const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
+            const uint32_t pa = sP + t * C::P_TILE_BYTES;
+            const uint32_t vb = sKV + vslot * C::KV_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              // A: P rows x 16 keys: key chunk kk/4 (16 KB apart), +32 B per 16 keys
+              const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+              // B: V 16 keys x D: +16 rows * 128 B per step; LBO = next 64-wide D chunk
+              const uint64_t bd = make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024);
+              mma_f16_ss(tm_o, ad, bd, IDESC_PV, (jj > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(bar_o_done(t));
+          }
+        }
+        mma_commit(bar_kv_empty(vslot));
+      };
+      for (int j = 0; j < nmax; ++j) {
+        const int k_slot = it % C::NST, k_use = it / C::NST;
+        ++it;
+        const int v_slot = it % C::NST, v_use = it / C::NST;
+        ++it;
+        mbar_wait(bar_kv_full(k_slot), k_use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) {
+          if (j < n_t[t]) {
+            if (j > 0) {
+              mbar_wait(bar_s_free(t), (j - 1) & 1);
+              tc_fence_after();
+            }
+            const uint32_t tm_s = tmem_base + t * BN;
+            const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
+            const uint32_t kb = sKV + k_slot * C::KV_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
+              mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
+                         make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(bar_s_full(t));
+          }
+        }
+        mma_commit(bar_kv_empty(k_slot));
+        if (j > 0) issue_pv(j - 1, v_slot_prev, v_use_prev);
+        v_slot_prev = v_slot;
+        v_use_prev = v_use;
+      }
+      issue_pv(nmax - 1, v_slot_prev, v_use_prev);
+    }
+    __syncwarp();
+  } else if (warp >= SOFTMAX_WARP0) {
+    // =========================== softmax / correction / epilogue ===========================
+    const int t = (warp - SOFTMAX_WARP0) >> 2;     // tile
+    const int q4 = warp & 3;                        // TMEM lane quarter this warp may access
+    const int lr = q4 * 32 + lane;                  // row within tile == TMEM lane
+    const int r0 = m_blk * (TILES * BM) + t * BM;
+    const int row = r0 + lr;                        // global query index
+    const int nt = n_t[t];
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t tm_s = tmem_base + lane_off + t * BN;
+    const uint32_t tm_o = tmem_base + lane_off + C::TMEM_O + t * D;
+    const uint32_t p_row = sP + t * C::P_TILE_BYTES + lr * 128;
+    const float c = p.c_log2;
+    // last key index this row may attend to (inclusive)
+    const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
+
+    float m = -INFINITY;  // running max of c * s   (scores_max; R2)
+    float l = 0.f;        // running sum            (logsum)
+
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(bar_s_full(t), j & 1);
+      tc_fence_after();
+      float s[BN];
+      {
+        uint32_t* sr = reinterpret_cast<uint32_t*>(s);
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc)
+          tmem_ld32(tm_s + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + cc * 32));
+        tmem_ld_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_s_free(t));  // S_t may be overwritten by the next QK^T
+
+      const int k0 = j * BN;
+      const bool masked = (k0 + BN - 1 > limit);  // any column beyond this row's limit
+      if (__any_sync(0xffffffffu, masked)) {
+#pragma unroll
+        for (int cc = 0; cc < BN; ++cc)
+          if (k0 + cc > limit) s[cc] = -INFINITY;
+      }
+      // row max (T.reduce_max): in-thread, the thread owns the whole row
+      float mx = s[0];
+#pragma unroll
+      for (int cc = 1; cc < BN; ++cc) mx = fmaxf(mx, s[cc]);
+      const float m_new = fmaxf(m, (mx == -INFINITY) ? -INFINITY : mx * c);
+      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
+      const float alpha = ex2(m - m_use);                      // scores_scale
+      // p = exp2(s*c - m), row sum from unrounded fp32 p (R8)
+      float sum = 0.f;
+      uint32_t pk[BN / 2];
+#pragma unroll
+      for (int cc = 0; cc < BN; cc += 2) {
+        float p0 = ex2(fmaf(s[cc], c, -m_use));
+        float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
+        if (s[cc] == -INFINITY) p0 = 0.f;
+        if (s[cc + 1] == -INFINITY) p1 = 0.f;
+        sum += p0 + p1;
+        pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype
+      }
+      if (j > 0) {
+        // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
+        mbar_wait(bar_o_done(t), (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // acc_o *= scores_scale
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t ov[32];
+            tmem_ld32(tm_o + cc * 32, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st32(tm_o + cc * 32, ov);
+          }
+          tmem_st_wait();
+        }
+      }
+      // P row -> smem, K-major SWIZZLE_128B: 16-B unit u of 64-key chunk goes to u ^ (row & 7)
+#pragma unroll
+      for (int ch = 0; ch < BN / 64; ++ch) {
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu) {
+          const uint32_t addr = p_row + ch * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
+          const int w = ch * 32 + uu * 4;
+          st_shared_v4(addr, pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_p_full(t));
+      l = l * alpha + sum;  // logsum = logsum * scores_scale + scores_sum
+      m = m_new;
+    }
+
+    // ---- epilogue: O / l, LSE, store
+    if (nt > 0) {
+      mbar_wait(bar_o_done(t), (nt - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
+    const bool row_ok = row < p.Sq;
+    uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
+                    ((((size_t)b * p.Sq + (row_ok ? row : 0)) * p.Hq + h) * D) * 2;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t ov[32];
+      if (nt > 0) {
+        tmem_ld32(tm_o + cc * 32, ov);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ov[e] = 0u;
+      }
+      uint32_t pkd[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
+      if (row_ok) {
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4)
+          st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2], pkd[4 * v4 + 3]);
+      }
+    }
+    if (p.lse != nullptr && row_ok) {
+      // lse = ln(sum exp(scale*s)) = (m + log2 l) * ln 2 with m in log2 units
+      p.lse[((size_t)b * p.Hq + h) * p.Sq + row] =
+          (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+    }
+    tc_fence_before();
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace tlattn

@@ -1,0 +1,295 @@
+// tlattn_api.cu — host side of libtlattn: the C ABI declared in include/tlattn.h.
+//
+// Argument validation happens before any CUDA call (TL_ERR_* returned synchronously,
+// nothing launched). Tensor maps are encoded per call (cheap host work, no device
+// allocation) and passed to the kernel as __grid_constant__ parameters, so the call is
+// CUDA-graph capturable. cuTensorMapEncodeTiled is resolved through the runtime's
+// driver entry point (no -lcuda link).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/tlattn.h"
+#include "attn_fwd_sm100.cuh"
+
+using namespace tlattn;
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+struct DeviceInfo {
+  int sm_count = 0;
+  int major = 0, minor = 0;
+  bool ok = false;
+  bool smem_set[4] = {false, false, false, false};
+};
+
+constexpr int kMaxDevices = 64;
+std::mutex g_mu;
+DeviceInfo g_dev[kMaxDevices];
+bool g_dev_init[kMaxDevices] = {};
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  return g_encode;
+}
+
+// Returns TL_OK and fills *dev, or an error code.
+int current_device(int* dev_out, DeviceInfo** info_out) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceInfo& di = g_dev[dev];
+  if (!g_dev_init[dev]) {
+    if (cudaDeviceGetAttribute(&di.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&di.major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&di.minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return TL_ERR_CUDA;
+    }
+    di.ok = (di.major == 10 && di.minor == 0);  // sm_100a code runs on sm_100 only
+    g_dev_init[dev] = true;
+  }
+  *dev_out = dev;
+  *info_out = &di;
+  return di.ok ? TL_OK : TL_ERR_UNSUPPORTED;
+}
+
+int validate(const void* q, const void* k, const void* v, const void* o, const float* lse, int B,
+             int Hq, int Hkv, int Sq, int Skv, int D, int causal, float scale, int dtype) {
+  if (!q || !k || !v || !o) return TL_ERR_INVALID_VALUE;
+  if (B < 1 || Hq < 1 || Hkv < 1 || Sq < 1 || Skv < 1 || D < 1) return TL_ERR_INVALID_VALUE;
+  if (causal != 0 && causal != 1) return TL_ERR_INVALID_VALUE;
+  if (!std::isfinite(scale)) return TL_ERR_INVALID_VALUE;
+  if (dtype != TL_DTYPE_F16 && dtype != TL_DTYPE_BF16) return TL_ERR_INVALID_VALUE;
+  if (D != 64 && D != 128) return TL_ERR_UNSUPPORTED;
+  if (Hq % Hkv != 0) return TL_ERR_UNSUPPORTED;
+  auto al = [](const void* ptr, uintptr_t a) { return (reinterpret_cast<uintptr_t>(ptr) % a) == 0; };
+  if (!al(q, 16) || !al(k, 16) || !al(v, 16) || !al(o, 16)) return TL_ERR_UNSUPPORTED;
+  if (lse && !al(lse, 4)) return TL_ERR_UNSUPPORTED;
+  // grid.x = B * Hq * ceil(Sq/256) must fit in int32; TMA coordinates are int32
+  const long long units = (long long)B * Hq * ((Sq + 255) / 256);
+  if (units > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
+  return TL_OK;
+}
+
+bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
+                 int Bn, int S, int H, int D) {
+  const cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)Bn};
+  const cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2,
+                                 (cuuint64_t)S * H * D * 2};
+  const cuuint32_t box[4] = {64, 1, 128, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int D, bool BF16>
+int launch(const AttnParams& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
+  auto kern = tl_attn_fwd_kernel<D, BF16>;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di.smem_set[inst]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               KCfg<D>::SMEM_BYTES) != cudaSuccess) {
+        cudaGetLastError();
+        return TL_ERR_CUDA;
+      }
+      di.smem_set[inst] = true;
+    }
+  }
+  kern<<<prm.n_units, NUM_THREADS, KCfg<D>::SMEM_BYTES, stream>>>(prm);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  return TL_OK;
+}
+
+}  // namespace
+
+extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B,
+                           int Hq, int Hkv, int Sq, int Skv, int D, int causal, float scale,
+                           int dtype, void* stream) {
+  g_last_launches = 0;
+  int rc = validate(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype);
+  if (rc != TL_OK) return rc;
+  int dev;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+
+  AttnParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (!encode_bshd(enc, &prm.tm_q, q, dtype, B, Sq, Hq, D) ||
+      !encode_bshd(enc, &prm.tm_k, k, dtype, B, Skv, Hkv, D) ||
+      !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D))
+    return TL_ERR_CUDA;
+  prm.o = o;
+  prm.lse = lse;
+  prm.B = B;
+  prm.Hq = Hq;
+  prm.Hkv = Hkv;
+  prm.Sq = Sq;
+  prm.Skv = Skv;
+  prm.causal = causal;
+  prm.c_log2 = std::fabs(scale) * 1.4426950408889634f;
+  prm.n_mblk = (Sq + TILES * BM - 1) / (TILES * BM);
+  prm.n_units = B * Hq * prm.n_mblk;
+  // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
+  // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
+  prm.neg = scale < 0.f ? 1 : 0;
+
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool bf = dtype == TL_DTYPE_BF16;
+  if (D == 128) rc = bf ? launch<128, true>(prm, *di, 0, st) : launch<128, false>(prm, *di, 1, st);
+  else rc = bf ? launch<64, true>(prm, *di, 2, st) : launch<64, false>(prm, *di, 3, st);
+  if (rc == TL_OK) g_last_launches = 1;
+  return rc;
+}
+
+// ------------------------------------------------------------------ host-buffer entry
+namespace {
+struct HostPlan {
+  int cb;             // batches per chunk
+  size_t q_b, kv_b, o_b, lse_b;  // bytes per batch element
+  size_t slot_bytes;  // one chunk slot (q, k, v, o, lse), 256-B aligned pieces
+};
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+HostPlan plan_host(int B, int Hq, int Hkv, int Sq, int Skv, int D, int with_lse) {
+  HostPlan pl;
+  pl.cb = B <= 2 ? B : (B + 7) / 8;  // ~8 chunks so copies overlap compute
+  pl.q_b = (size_t)Sq * Hq * D * 2;
+  pl.kv_b = (size_t)Skv * Hkv * D * 2;
+  pl.o_b = pl.q_b;
+  pl.lse_b = with_lse ? (size_t)Hq * Sq * 4 : 0;
+  pl.slot_bytes = al256(pl.cb * pl.q_b) + 2 * al256(pl.cb * pl.kv_b) + al256(pl.cb * pl.o_b) +
+                  al256(pl.cb * pl.lse_b);
+  return pl;
+}
+
+std::mutex g_stream_mu;
+cudaStream_t g_copy_streams[kMaxDevices][2] = {};
+}  // namespace
+
+extern "C" uint64_t tl_attn_host_workspace_bytes(int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                                                 int with_lse) {
+  if (B < 1 || Hq < 1 || Hkv < 1 || Sq < 1 || Skv < 1 || D < 1) return 0;
+  HostPlan pl = plan_host(B, Hq, Hkv, Sq, Skv, D, with_lse);
+  return 2 * (uint64_t)pl.slot_bytes;
+}
+
+extern "C" int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_h, void* o_h,
+                                float* lse_h, int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                                int causal, float scale, int dtype, void* ws, uint64_t ws_bytes,
+                                void* stream) {
+  g_last_launches = 0;
+  int rc = validate(q_h, k_h, v_h, o_h, lse_h, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype);
+  if (rc != TL_OK) return rc;
+  if (!ws) return TL_ERR_INVALID_VALUE;
+  HostPlan pl = plan_host(B, Hq, Hkv, Sq, Skv, D, lse_h != nullptr);
+  if (ws_bytes < 2 * (uint64_t)pl.slot_bytes) return TL_ERR_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(ws) % 256 != 0) return TL_ERR_UNSUPPORTED;
+  int dev;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t h2d, d2h;
+  {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    for (int i = 0; i < 2; ++i)
+      if (!g_copy_streams[dev][i] &&
+          cudaStreamCreateWithFlags(&g_copy_streams[dev][i], cudaStreamNonBlocking) != cudaSuccess)
+        return TL_ERR_CUDA;
+    h2d = g_copy_streams[dev][0];
+    d2h = g_copy_streams[dev][1];
+  }
+  const int nchunks = (B + pl.cb - 1) / pl.cb;
+  cudaEvent_t ev_start, ev_in[2], ev_comp[2], ev_out[2];
+  auto mk = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
+  if (!mk(&ev_start)) return TL_ERR_CUDA;
+  for (int i = 0; i < 2; ++i)
+    if (!mk(&ev_in[i]) || !mk(&ev_comp[i]) || !mk(&ev_out[i])) return TL_ERR_CUDA;
+  bool ok = cudaEventRecord(ev_start, cs) == cudaSuccess;
+  ok = ok && cudaStreamWaitEvent(h2d, ev_start, 0) == cudaSuccess;
+  int launches = 0;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  for (int c = 0; c < nchunks && ok; ++c) {
+    const int s = c & 1;
+    const int b0 = c * pl.cb;
+    const int nb = (B - b0) < pl.cb ? (B - b0) : pl.cb;
+    uint8_t* slot = wsb + (size_t)s * pl.slot_bytes;
+    uint8_t* dq = slot;
+    uint8_t* dk = dq + al256(pl.cb * pl.q_b);
+    uint8_t* dv = dk + al256(pl.cb * pl.kv_b);
+    uint8_t* dout = dv + al256(pl.cb * pl.kv_b);
+    float* dlse = lse_h ? reinterpret_cast<float*>(dout + al256(pl.cb * pl.o_b)) : nullptr;
+    if (c >= 2) ok = ok && cudaStreamWaitEvent(h2d, ev_out[s], 0) == cudaSuccess;  // slot free
+    ok = ok && cudaMemcpyAsync(dq, (const uint8_t*)q_h + (size_t)b0 * pl.q_b, nb * pl.q_b, cudaMemcpyHostToDevice, h2d) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(dk, (const uint8_t*)k_h + (size_t)b0 * pl.kv_b, nb * pl.kv_b, cudaMemcpyHostToDevice, h2d) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(dv, (const uint8_t*)v_h + (size_t)b0 * pl.kv_b, nb * pl.kv_b, cudaMemcpyHostToDevice, h2d) == cudaSuccess;
+    ok = ok && cudaEventRecord(ev_in[s], h2d) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(cs, ev_in[s], 0) == cudaSuccess;
+    if (!ok) break;
+    rc = tl_attn_fwd(dq, dk, dv, dout, dlse, nb, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, cs);
+    if (rc != TL_OK) break;
+    ++launches;
+    ok = ok && cudaEventRecord(ev_comp[s], cs) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(d2h, ev_comp[s], 0) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync((uint8_t*)o_h + (size_t)b0 * pl.o_b, dout, nb * pl.o_b, cudaMemcpyDeviceToHost, d2h) == cudaSuccess;
+    if (lse_h)
+      ok = ok && cudaMemcpyAsync((uint8_t*)lse_h + (size_t)b0 * pl.lse_b, dlse, nb * pl.lse_b, cudaMemcpyDeviceToHost, d2h) == cudaSuccess;
+    ok = ok && cudaEventRecord(ev_out[s], d2h) == cudaSuccess;
+  }
+  // caller's stream resumes after the last device->host copy
+  if (ok && rc == TL_OK) ok = cudaStreamWaitEvent(cs, ev_out[(nchunks - 1) & 1], 0) == cudaSuccess;
+  cudaEventDestroy(ev_start);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_comp[i]);
+    cudaEventDestroy(ev_out[i]);
+  }
+  if (rc != TL_OK) return rc;
+  if (!ok) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  g_last_launches = launches;
+  return TL_OK;
+}
+
+extern "C" const char* tl_attn_strerror(int status) {
+  switch (status) {
+    case TL_OK: return "TL_OK: success";
+    case TL_ERR_INVALID_VALUE: return "TL_ERR_INVALID_VALUE: invalid argument (null pointer, size < 1, causal not 0/1, non-finite scale, unknown dtype, or workspace too small)";
+    case TL_ERR_UNSUPPORTED: return "TL_ERR_UNSUPPORTED: unsupported configuration (D not 64/128, Hq % Hkv != 0, misaligned pointer, size limit, or device is not sm_100)";
+    case TL_ERR_CUDA: return "TL_ERR_CUDA: a CUDA runtime/driver call failed";
+    default: return "unknown tl_status code";
+  }
+}
+
+extern "C" int tl_attn_version(void) { return TLATTN_VERSION; }
+
+extern "C" int tl_attn_last_launch_count(void) { return g_last_launches; }

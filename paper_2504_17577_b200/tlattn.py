@@ -1,0 +1,176 @@
+"""Thin Python binding of libtlattn (include/tlattn.h): argument marshalling only.
+
+Every step of the attention forward runs in the CUDA kernels of libtlattn.so; this
+module only turns torch tensors into pointers/sizes and raises on error codes.
+PyTorch is used for device memory and streams. There is no CPU fallback: if the
+library is missing or the device is not sm_100 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+import torch
+
+from .build import LIB
+
+TL_DTYPE_F16 = 0
+TL_DTYPE_BF16 = 1
+TL_OK, TL_ERR_INVALID_VALUE, TL_ERR_UNSUPPORTED, TL_ERR_CUDA = 0, 1, 2, 3
+
+_lock = threading.Lock()
+_lib = None
+
+
+class TlAttnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+def load_library(path: str | None = None):
+    """Load libtlattn.so (in-tree). Raises if it has not been built."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = path or LIB
+        if not os.path.exists(path):
+            raise RuntimeError(f"libtlattn.so not found at {path}: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        I, F, P, U64 = ctypes.c_int, ctypes.c_float, ctypes.c_void_p, ctypes.c_uint64
+        lib.tl_attn_fwd.argtypes = [P, P, P, P, P, I, I, I, I, I, I, I, F, I, P]
+        lib.tl_attn_fwd.restype = I
+        lib.tl_attn_fwd_host.argtypes = [P, P, P, P, P, I, I, I, I, I, I, I, F, I, P, U64, P]
+        lib.tl_attn_fwd_host.restype = I
+        lib.tl_attn_host_workspace_bytes.argtypes = [I, I, I, I, I, I, I]
+        lib.tl_attn_host_workspace_bytes.restype = U64
+        lib.tl_attn_strerror.argtypes = [I]
+        lib.tl_attn_strerror.restype = ctypes.c_char_p
+        lib.tl_attn_version.argtypes = []
+        lib.tl_attn_version.restype = I
+        lib.tl_attn_last_launch_count.argtypes = []
+        lib.tl_attn_last_launch_count.restype = I
+        _lib = lib
+        return lib
+
+
+def tl_attn_strerror(status: int) -> str:
+    return load_library().tl_attn_strerror(int(status)).decode()
+
+
+def tl_attn_version() -> int:
+    return load_library().tl_attn_version()
+
+
+def tl_attn_last_launch_count() -> int:
+    return load_library().tl_attn_last_launch_count()
+
+
+def _check(rc: int):
+    if rc != TL_OK:
+        raise TlAttnError(rc, tl_attn_strerror(rc))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float16:
+        return TL_DTYPE_F16
+    if dt == torch.bfloat16:
+        return TL_DTYPE_BF16
+    raise TlAttnError(TL_ERR_INVALID_VALUE, f"unsupported dtype {dt}")
+
+
+def tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, stream=None):
+    """Direct mirror of the C entry point (device pointers or tensors)."""
+    _check(load_library().tl_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                      int(B), int(Hq), int(Hkv), int(Sq), int(Skv), int(D),
+                                      int(causal), float(scale), int(dtype),
+                                      _stream_handle(stream) if not isinstance(stream, int) else stream))
+
+
+def tl_attn_host_workspace_bytes(B, Hq, Hkv, Sq, Skv, D, with_lse=True) -> int:
+    return int(load_library().tl_attn_host_workspace_bytes(B, Hq, Hkv, Sq, Skv, D, int(with_lse)))
+
+
+def tl_attn_fwd_host(q_h, k_h, v_h, o_h, lse_h, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype,
+                     ws, ws_bytes, stream=None):
+    """Direct mirror of the C host-buffer entry point."""
+    _check(load_library().tl_attn_fwd_host(_ptr(q_h), _ptr(k_h), _ptr(v_h), _ptr(o_h), _ptr(lse_h),
+                                           int(B), int(Hq), int(Hkv), int(Sq), int(Skv), int(D),
+                                           int(causal), float(scale), int(dtype), _ptr(ws),
+                                           int(ws_bytes), _stream_handle(stream)))
+
+
+def _dims(q, k, v):
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4 or k.shape != v.shape:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "expected BSHD q[B,Sq,Hq,D], k/v[B,Skv,Hkv,D]")
+    B, Sq, Hq, D = q.shape
+    Bk, Skv, Hkv, Dk = k.shape
+    if Bk != B or Dk != D or q.dtype != k.dtype or q.dtype != v.dtype:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "q/k/v batch, head_dim or dtype mismatch")
+    for t in (q, k, v):
+        if not t.is_contiguous():
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "q/k/v must be contiguous BSHD")
+    return B, Hq, Hkv, Sq, Skv, D
+
+
+def attention(q, k, v, causal=False, scale=None, return_lse=True, out=None, lse_out=None,
+              stream=None):
+    """o[, lse] = softmax(scale q k^T [+ causal mask]) v on the GPU (allocates outputs)."""
+    B, Hq, Hkv, Sq, Skv, D = _dims(q, k, v)
+    if not q.is_cuda:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "attention() takes CUDA tensors; use "
+                          "attention_host() for host buffers")
+    scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+    o = out if out is not None else torch.empty_like(q)
+    lse = None
+    if return_lse:
+        lse = lse_out if lse_out is not None else torch.empty((B, Hq, Sq), dtype=torch.float32,
+                                                              device=q.device)
+    tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, int(bool(causal)), scale,
+                dtype_code(q.dtype), stream)
+    return (o, lse) if return_lse else o
+
+
+class HostAttention:
+    """End-to-end entry on HOST (ideally pinned) tensors via tl_attn_fwd_host.
+
+    Holds the device workspace for one problem shape (allocated by torch).
+    """
+
+    def __init__(self, B, Hq, Hkv, Sq, Skv, D, with_lse=True, device=None):
+        self.shape = (B, Hq, Hkv, Sq, Skv, D)
+        self.with_lse = with_lse
+        nbytes = tl_attn_host_workspace_bytes(B, Hq, Hkv, Sq, Skv, D, with_lse)
+        if nbytes == 0:
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "bad problem size")
+        self.ws_bytes = nbytes
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+
+    def __call__(self, q_h, k_h, v_h, o_h, lse_h=None, causal=False, scale=None, stream=None):
+        B, Hq, Hkv, Sq, Skv, D = self.shape
+        if _dims(q_h, k_h, v_h) != self.shape:
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "shape differs from this HostAttention's")
+        scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+        tl_attn_fwd_host(q_h, k_h, v_h, o_h, lse_h if self.with_lse else None, B, Hq, Hkv, Sq,
+                         Skv, D, int(bool(causal)), scale, dtype_code(q_h.dtype), self.ws,
+                         self.ws_bytes, stream)

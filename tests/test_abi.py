@@ -1,0 +1,105 @@
+"""C-ABI checks that need no GPU: the library builds/loads, exports every symbol
+include/tlattn.h declares, and rejects bad arguments synchronously BEFORE any CUDA
+call (include/tlattn.h "Errors")."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from paper_2504_17577_b200 import build as pkg_build
+from paper_2504_17577_b200 import tlattn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tlattn.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    pkg_build.build()
+    return tlattn.load_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tl_attn_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_entry_points():
+    names = declared_functions()
+    for n in ("tl_attn_fwd", "tl_attn_fwd_host", "tl_attn_host_workspace_bytes",
+              "tl_attn_strerror", "tl_attn_version", "tl_attn_last_launch_count"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    raw = ctypes.CDLL(pkg_build.LIB)
+    for name in declared_functions():
+        assert hasattr(raw, name), f"libtlattn.so does not export {name}"
+
+
+def test_version_and_strerror(lib):
+    assert tlattn.tl_attn_version() == 0x000100
+    for code in (0, 1, 2, 3):
+        assert tlattn.tl_attn_strerror(code).startswith(("TL_OK", "TL_ERR"))
+    assert "unknown" in tlattn.tl_attn_strerror(99)
+
+
+FAKE = 1 << 20  # a 16-byte-aligned non-null "device pointer" (never dereferenced)
+
+GOOD = dict(q=FAKE, k=FAKE, v=FAKE, o=FAKE, lse=FAKE, B=1, Hq=2, Hkv=1, Sq=128, Skv=128, D=128,
+            causal=0, scale=0.125, dtype=1)
+
+
+def call(lib, **over):
+    a = dict(GOOD, **over)
+    return lib.tl_attn_fwd(a["q"], a["k"], a["v"], a["o"], a["lse"], a["B"], a["Hq"], a["Hkv"],
+                           a["Sq"], a["Skv"], a["D"], a["causal"], a["scale"], a["dtype"], None)
+
+
+@pytest.mark.parametrize("over,code", [
+    (dict(q=None), 1), (dict(k=None), 1), (dict(v=None), 1), (dict(o=None), 1),
+    (dict(B=0), 1), (dict(Hq=0), 1), (dict(Hkv=-1), 1), (dict(Sq=0), 1), (dict(Skv=0), 1),
+    (dict(D=0), 1), (dict(causal=2), 1), (dict(scale=float("nan")), 1),
+    (dict(scale=float("inf")), 1), (dict(dtype=5), 1),
+    (dict(D=96), 2), (dict(D=256), 2), (dict(Hq=3, Hkv=2), 2), (dict(q=FAKE + 8), 2),
+    (dict(o=FAKE + 2), 2), (dict(lse=FAKE + 2), 2),
+    (dict(B=1 << 20, Hq=1 << 10, Hkv=1 << 10, Sq=1 << 12), 2),
+])
+def test_invalid_arguments_rejected(lib, over, code):
+    assert call(lib, **over) == code
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_valid_arguments_without_device_is_cuda_error(lib):
+    # Validation passes; the first CUDA call finds no device -> TL_ERR_CUDA, no fallback.
+    assert call(lib) == 3
+    assert call(lib, lse=None) == 3
+
+
+def test_host_workspace_size(lib):
+    n = tlattn.tl_attn_host_workspace_bytes(64, 32, 32, 2048, 2048, 128, True)
+    per_b = 2048 * 32 * 128 * 2
+    assert n >= 2 * (4 * per_b) * 8 and n % 256 == 0
+    assert tlattn.tl_attn_host_workspace_bytes(0, 1, 1, 1, 1, 64, True) == 0
+
+
+def test_host_entry_rejects_small_workspace(lib):
+    rc = lib.tl_attn_fwd_host(FAKE, FAKE, FAKE, FAKE, None, 1, 1, 1, 128, 128, 64, 0, 0.1, 0,
+                              FAKE, 16, None)
+    assert rc == 1
+    rc = lib.tl_attn_fwd_host(FAKE, FAKE, FAKE, FAKE, None, 1, 1, 1, 128, 128, 64, 0, 0.1, 0,
+                              None, 1 << 30, None)
+    assert rc == 1
+
+
+def test_python_binding_fails_loudly_without_library(tmp_path):
+    with pytest.raises(RuntimeError):
+        saved = tlattn._lib
+        tlattn._lib = None
+        try:
+            tlattn.load_library(str(tmp_path / "missing.so"))
+        finally:
+            tlattn._lib = saved

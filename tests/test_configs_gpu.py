@@ -1,0 +1,30 @@
+"""Parity on the five BASELINE.json configs (+ T0) at full size, in the launch
+configuration bench.py times (one tl_attn_fwd call over the whole problem).
+
+C1 is checked on every element. C2..C5 and T0 are checked on sampled rows the oracle
+computes one by one: rows 0..63, tile/unit boundaries and the last 16 rows of EVERY
+(b, h), plus every row of two (b, h) pairs and 256 random rows.
+"""
+import numpy as np
+import pytest
+
+from paper_2504_17577_b200.configs import CONFIGS
+
+from _parity import check_against_oracle, gen, sample_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5", "T0"])
+def test_config_parity(name):
+    cfg = CONFIGS[name]
+    q, k, v = gen(cfg.B, cfg.Hq, cfg.Hkv, cfg.Sq, cfg.Skv, cfg.D, cfg.dtype, cfg.seed)
+    rng = np.random.default_rng(cfg.seed)
+    if name == "C1":
+        stats, _ = check_against_oracle(q, k, v, cfg.causal, cfg.scale, label=name)
+    else:
+        rows = sample_rows(cfg.Sq, rng, extra=256)
+        full = ((0, 0), (cfg.B - 1, cfg.Hq - 1))
+        stats, _ = check_against_oracle(q, k, v, cfg.causal, cfg.scale, rows_per_head=rows,
+                                        label=name, full_rows_heads=full)
+    print(name, stats)

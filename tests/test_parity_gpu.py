@@ -1,0 +1,161 @@
+"""GPU parity: libtlattn (through the C ABI) vs the fp64 oracle, element by element.
+
+Small shapes are checked on every row; they span several 128-row tiles / 256-row
+units and ragged tails. Structured inputs pin masking, rescaling and GQA bitwise.
+The full BASELINE configs are in test_configs_gpu.py.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2504_17577_b200 import attention, tl_attn_last_launch_count
+from paper_2504_17577_b200.inputs import from_values, to_bits
+
+from _parity import check_against_oracle, default_scale, gen, odt
+
+pytestmark = pytest.mark.gpu
+
+BF, F16 = torch.bfloat16, torch.float16
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,Sq,Skv,D,dtype,causal", [
+    (1, 1, 1, 128, 128, 64, F16, False),      # C1 shape
+    (1, 1, 1, 128, 128, 64, F16, True),
+    (2, 4, 2, 300, 300, 128, BF, False),      # ragged tails, 2 units, GQA
+    (2, 4, 2, 300, 300, 128, BF, True),
+    (1, 2, 1, 1000, 1000, 64, F16, True),     # ragged, many blocks
+    (1, 2, 2, 1000, 1000, 64, BF, False),
+    (1, 3, 3, 640, 640, 128, F16, True),
+    (1, 2, 1, 200, 520, 128, BF, True),       # Sq < Skv, causal bottom-right
+    (1, 2, 1, 520, 200, 128, BF, True),       # Sq > Skv: leading rows have no key
+    (1, 2, 1, 520, 200, 64, F16, False),
+    (2, 2, 2, 1, 1, 128, BF, False),          # single element
+    (1, 2, 2, 1, 777, 64, F16, True),         # one query row
+    (1, 1, 1, 129, 1, 128, BF, False),        # one key
+    (1, 4, 4, 257, 257, 128, BF, True),
+])
+def test_parity_small(B, Hq, Hkv, Sq, Skv, D, dtype, causal):
+    q, k, v = gen(B, Hq, Hkv, Sq, Skv, D, dtype, 7 + Sq + Skv)
+    stats, _ = check_against_oracle(q, k, v, causal, default_scale(D),
+                                    label=f"B{B} H{Hq}/{Hkv} S{Sq}x{Skv} D{D} {dtype} c{causal}")
+    assert tl_attn_last_launch_count() == 1
+    print(stats)
+
+
+@pytest.mark.parametrize("scale", [0.0, -0.125, 0.37])
+def test_scale_values(scale):
+    """scale is used literally: 0 (uniform attention) and negative values are legal."""
+    q, k, v = gen(1, 2, 1, 384, 384, 128, BF, 11)
+    check_against_oracle(q, k, v, True, scale, label=f"scale={scale}")
+
+
+@pytest.mark.parametrize("D,dtype", [(64, F16), (128, BF)])
+def test_causal_row0_is_v0_bitwise(D, dtype):
+    """Causal, Sq == Skv: row 0 attends only key 0: p = exp2(0) = 1, l = 1 -> O[0] == V[0]
+    bitwise and LSE[0] == scale * q0.k0."""
+    q, k, v = gen(2, 4, 2, 512, 512, D, dtype, 21)
+    o, lse = attention(q, k, v, causal=True)
+    torch.cuda.synchronize()
+    for h in range(4):
+        assert torch.equal(o[:, 0, h], v[:, 0, h // 2])
+    s00 = (q[:, 0].float() * k[:, 0].float().repeat_interleave(2, dim=1)).sum(-1) / math.sqrt(D)
+    torch.testing.assert_close(lse[:, :, 0], s00, atol=1e-4, rtol=1e-5)
+
+
+def test_hard_attention_gather_bitwise():
+    """K rows = +-64 e_{j mod D}, Q rows = +-64 e_{pi(i)}, D=128, S=256, scale=1/sqrt(D):
+    the score gap 4096*c (522 in log2 units) underflows every non-matching exp2 to 0,
+    so O_i == V_{pi(i)} bitwise and LSE_i = 4096*scale. Matches in block 1 exercise the
+    running-max rescale with alpha = 0."""
+    D, S = 128, 256
+    kv = np.zeros((1, S, 1, D), np.float32)
+    for j in range(S):
+        kv[0, j, 0, j % D] = 64.0 if j < D else -64.0
+    perm = np.random.default_rng(5).permutation(S)
+    qv = np.zeros((1, S, 1, D), np.float32)
+    for i in range(S):
+        qv[0, i, 0, perm[i] % D] = 64.0 if perm[i] < D else -64.0
+    q = from_values(qv, BF, "cuda")
+    k = from_values(kv, BF, "cuda")
+    _, _, v = gen(1, 1, 1, S, S, D, BF, 6)
+    o, lse = attention(q, k, v, causal=False)
+    torch.cuda.synchronize()
+    assert torch.equal(o[0, :, 0], v[0, perm, 0])
+    torch.testing.assert_close(lse[0, 0], torch.full((S,), 4096.0 / math.sqrt(D), device="cuda"),
+                               atol=1e-3, rtol=0)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_gqa_equals_repeated_mha_bitwise(causal):
+    """Hkv < Hq gives exactly the result of MHA with K/V heads repeated."""
+    q, k, v = gen(2, 8, 2, 384, 384, 128, BF, 31)
+    o1, l1 = attention(q, k, v, causal=causal)
+    kr = k.repeat_interleave(4, dim=2).contiguous()
+    vr = v.repeat_interleave(4, dim=2).contiguous()
+    o2, l2 = attention(q, kr, vr, causal=causal)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_equal_scores_give_mean_v(causal):
+    """Q = 0: all allowed scores are 0 -> O_i = mean of V over J_i, LSE_i = ln|J_i|."""
+    Sq = Skv = 300
+    q = torch.zeros(1, Sq, 2, 64, dtype=F16, device="cuda")
+    _, k, v = gen(1, 2, 2, Sq, Skv, 64, F16, 41)
+    o, lse = attention(q, k, v, causal=causal)
+    torch.cuda.synchronize()
+    cnt = torch.arange(1, Sq + 1, device="cuda", dtype=torch.float64) if causal else \
+        torch.full((Sq,), float(Skv), device="cuda", dtype=torch.float64)
+    vf = v.double()
+    ref = (vf.cumsum(1) / cnt[None, :, None, None]) if causal else vf.mean(1, keepdim=True).expand_as(vf)
+    torch.testing.assert_close(o.double(), ref, atol=2e-3, rtol=2e-3)
+    torch.testing.assert_close(lse.double(), cnt.log()[None, None, :].expand(1, 2, Sq), atol=1e-5, rtol=0)
+
+
+def test_deterministic():
+    q, k, v = gen(2, 4, 4, 700, 700, 128, BF, 51)
+    o1, l1 = attention(q, k, v, causal=True)
+    o2, l2 = attention(q, k, v, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_lse_optional_and_stream_ordered():
+    q, k, v = gen(1, 2, 2, 256, 256, 64, F16, 61)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        o = attention(q, k, v, causal=True, return_lse=False)
+    s.synchronize()
+    o2, _ = attention(q, k, v, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2)
+
+
+def test_host_entry_matches_device_entry():
+    """tl_attn_fwd_host (host buffers, chunked H2D/compute/D2H) == tl_attn_fwd."""
+    from paper_2504_17577_b200 import HostAttention
+    B, Hq, Hkv, S, D = 5, 4, 2, 384, 128
+    q, k, v = gen(B, Hq, Hkv, S, S, D, BF, 71)
+    o_ref, l_ref = attention(q, k, v, causal=True)
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    lh = torch.empty((B, Hq, S), dtype=torch.float32).pin_memory()
+    ha = HostAttention(B, Hq, Hkv, S, S, D, with_lse=True)
+    ha(qh, kh, vh, oh, lh, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, o_ref.cpu()) and torch.equal(lh, l_ref.cpu())
+    assert tl_attn_last_launch_count() >= 1
+
+
+def test_bad_args_raise_before_launch():
+    from paper_2504_17577_b200 import TlAttnError, tl_attn_fwd
+    q, k, v = gen(1, 2, 2, 128, 128, 96, BF, 1)  # D=96 unsupported
+    o = torch.empty_like(q)
+    with pytest.raises(TlAttnError) as e:
+        tl_attn_fwd(q, k, v, o, None, 1, 2, 2, 128, 128, 96, 0, 0.1, 1)
+    assert e.value.status == 2
+    _ = oracle, odt, to_bits  # imported for parity with the other GPU test modules
