@@ -60,9 +60,11 @@ struct KCfg {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + TILES * Q_TILE_BYTES;
   static constexpr int OFF_P = OFF_KV + NST * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_P + TILES * P_TILE_BYTES;
-  // barriers: q_full, kv_full[NST], kv_empty[NST], s_full[2], s_free[2], p_full[2], o_done[2]
-  static constexpr int NUM_BARS = 1 + 2 * NST + 8;
+  static constexpr int OFF_SCHED = OFF_P + TILES * P_TILE_BYTES;  // 2 x 16-B CLC responses
+  static constexpr int OFF_BAR = OFF_SCHED + 32;
+  // barriers: q_full, q_empty, kv_full[NST], kv_empty[NST], s_full[2], s_free[2], p_full[2],
+  //           o_done[2], sched_full[2], sched_empty[2]
+  static constexpr int NUM_BARS = 2 + 2 * NST + 12;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_USED = OFF_TMEMPTR + 16;
   static constexpr int SMEM_BYTES = SMEM_USED + 1024;  // slack for 1024-B alignment
@@ -92,51 +94,70 @@ __device__ __forceinline__ int tile_nblocks(int r0, const AttnParams& p) {
   return min(n_all, (int)(kmax / BN) + 1);
 }
 
+
+// Rescale O only when a row max grows by more than 2^RESCALE_LOG2:
+// otherwise keep the stale max, so p = exp2(c s - m) <= 2^8 stays well inside fp16/bf16
+// range and the result is unchanged up to rounding (O and l use the same m).
+constexpr float RESCALE_LOG2 = 8.0f;
+constexpr uint32_t REGS_SMALL = 88;     // warpgroup 0: 128 x 88
+constexpr uint32_t REGS_SOFTMAX = 208;  // warpgroups 1-2: 256 x 208 (total 64512 <= 64K)
+
+struct Unit {
+  int b, h, hkv, m_blk, n0, n1;
+};
+
+// Unit order: (b, h) major, 256-row query block minor; causal: heaviest block first.
+// Units of one (b, kv-head) group are adjacent in launch (= CLC steal) order, so their
+// K/V stay L2-resident (the T.use_swizzle idea).
+__device__ __forceinline__ Unit decode_unit(int u, const AttnParams& p) {
+  Unit U;
+  const int mb_i = u % p.n_mblk;
+  const int bh = u / p.n_mblk;
+  U.h = bh % p.Hq;
+  U.b = bh / p.Hq;
+  U.m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
+  U.hkv = U.h / (p.Hq / p.Hkv);  // GQA grouping
+  U.n0 = tile_nblocks(U.m_blk * (TILES * BM), p);
+  U.n1 = tile_nblocks(U.m_blk * (TILES * BM) + BM, p);
+  return U;
+}
+
 template <int D, bool BF16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   using C = KCfg<D>;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned base (SWIZZLE_128B atoms)
   const uint32_t raw_u32 = smem_u32(smem_raw);
-  const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+  const uint32_t base = (raw_u32 + 1023u) & ~1023u;  // 1024-B aligned (SWIZZLE_128B atoms)
   uint8_t* smem = smem_raw + (base - raw_u32);
 
   const uint32_t sQ = base + C::OFF_Q;
   const uint32_t sKV = base + C::OFF_KV;
   const uint32_t sP = base + C::OFF_P;
+  const uint32_t sSched = base + C::OFF_SCHED;
   const uint32_t bar0 = base + C::OFF_BAR;
   const uint32_t bar_q_full = bar0;
-  auto bar_kv_full = [&](int s) { return bar0 + 8u * (1 + s); };
-  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (1 + C::NST + s); };
-  auto bar_s_full = [&](int t) { return bar0 + 8u * (1 + 2 * C::NST + t); };
-  auto bar_s_free = [&](int t) { return bar0 + 8u * (3 + 2 * C::NST + t); };
-  auto bar_p_full = [&](int t) { return bar0 + 8u * (5 + 2 * C::NST + t); };
-  auto bar_o_done = [&](int t) { return bar0 + 8u * (7 + 2 * C::NST + t); };
+  const uint32_t bar_q_empty = bar0 + 8u;
+  auto bar_kv_full = [&](int s) { return bar0 + 8u * (2 + s); };
+  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (2 + C::NST + s); };
+  auto bar_s_full = [&](int t) { return bar0 + 8u * (2 + 2 * C::NST + t); };
+  auto bar_s_free = [&](int t) { return bar0 + 8u * (4 + 2 * C::NST + t); };
+  auto bar_p_full = [&](int t) { return bar0 + 8u * (6 + 2 * C::NST + t); };
+  auto bar_o_done = [&](int t) { return bar0 + 8u * (8 + 2 * C::NST + t); };
+  auto bar_sched_full = [&](int i) { return bar0 + 8u * (10 + 2 * C::NST + i); };
+  auto bar_sched_empty = [&](int i) { return bar0 + 8u * (12 + 2 * C::NST + i); };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- unit decode: (b, h) major, query block minor; causal: heaviest block first
-  const int u = blockIdx.x;
-  const int mb_i = u % p.n_mblk;
-  const int bh = u / p.n_mblk;
-  const int h = bh % p.Hq;
-  const int b = bh / p.Hq;
-  const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
-  const int hkv = h / (p.Hq / p.Hkv);  // GQA grouping
-  int n_t[TILES];
-#pragma unroll
-  for (int t = 0; t < TILES; ++t) n_t[t] = tile_nblocks(m_blk * (TILES * BM) + t * BM, p);
-  const int nmax = max(n_t[0], n_t[1]);
-
-  // ---- setup
+  // ---- setup (once per persistent CTA)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tm_q);
     prefetch_tmap(&p.tm_k);
     prefetch_tmap(&p.tm_v);
     mbar_init(bar_q_full, 1);
+    mbar_init(bar_q_empty, 1);
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(bar_kv_full(s), 1);
       mbar_init(bar_kv_empty(s), 1);
@@ -147,6 +168,10 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
       mbar_init(bar_p_full(t), 4);
       mbar_init(bar_o_done(t), 1);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_sched_full(i), 1);
+      mbar_init(bar_sched_empty(i), 1 + 8);  // MMA thread + 8 softmax warps
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_ptr_smem));
@@ -155,242 +180,301 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_smem;
 
+  // Register rebalancing: warpgroup 0 (load / MMA / spare warps) gives registers to the
+  // two softmax warpgroups, which hold a 128-column fp32 S row per thread.
+  if (warp < 4) {
+  setmaxnreg_dec<REGS_SMALL>();
   if (warp == 0) {
-    // =========================== TMA producer ===========================
+    // =========================== TMA producer + CLC scheduler ===========================
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      uint32_t qbytes = 0;
+      int unit = blockIdx.x;
+      int it = 0;  // K/V ring position (K_j, V_j alternate)
+      for (int k = 0;; ++k) {
+        // ask for the next unit now; the answer is needed only at the end of this one
+        const int sl = k & 1;
+        if (k >= 2) mbar_wait(bar_sched_empty(sl), ((k >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(bar_sched_full(sl), 16);
+        clc_try_cancel(sSched + 16 * sl, bar_sched_full(sl));
+
+        const Unit U = decode_unit(unit, p);
+        const int nmax = max(U.n0, U.n1);
+        const int r00 = U.m_blk * (TILES * BM);
+        if (k >= 1) mbar_wait(bar_q_empty, (k - 1) & 1);  // previous unit's QK^T done
+        uint32_t qbytes = 0;
 #pragma unroll
-      for (int t = 0; t < TILES; ++t)
-        if (m_blk * (TILES * BM) + t * BM < p.Sq) qbytes += C::Q_TILE_BYTES;
-      mbar_arrive_expect_tx(bar_q_full, qbytes);
+        for (int t = 0; t < TILES; ++t)
+          if (r00 + t * BM < p.Sq) qbytes += C::Q_TILE_BYTES;
+        mbar_arrive_expect_tx(bar_q_full, qbytes);
 #pragma unroll
-      for (int t = 0; t < TILES; ++t) {
-        const int r0 = m_blk * (TILES * BM) + t * BM;
-        if (r0 < p.Sq) {
+        for (int t = 0; t < TILES; ++t) {
+          if (r00 + t * BM < p.Sq) {
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c)
-            tma_load_4d(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, bar_q_full, c * 64,
-                        h, r0, b, pol_q);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, bar_q_full, c * 64,
+                          U.h, r00 + t * BM, U.b, pol_q);
+          }
         }
-      }
-      int it = 0;
-      for (int j = 0; j < nmax; ++j) {
+        for (int j = 0; j < nmax; ++j) {
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv, ++it) {
-          const int slot = it % C::NST;
-          const int use = it / C::NST;
-          if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
-          mbar_arrive_expect_tx(bar_kv_full(slot), C::KV_BYTES);
+          for (int kv = 0; kv < 2; ++kv, ++it) {
+            const int slot = it % C::NST;
+            const int use = it / C::NST;
+            if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
+            mbar_arrive_expect_tx(bar_kv_full(slot), C::KV_BYTES);
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c)
-            tma_load_4d(sKV + slot * C::KV_BYTES + c * CHUNK_BYTES, kv == 0 ? &p.tm_k : &p.tm_v,
-                        bar_kv_full(slot), c * 64, hkv, j * BN, b, pol_kv);
+            for (int c = 0; c < D / 64; ++c)
+              tma_load_4d(sKV + slot * C::KV_BYTES + c * CHUNK_BYTES, kv == 0 ? &p.tm_k : &p.tm_v,
+                          bar_kv_full(slot), c * 64, U.hkv, j * BN, U.b, pol_kv);
+          }
         }
+        mbar_wait(bar_sched_full(sl), (k >> 1) & 1);
+        const int nxt = clc_query(sSched + 16 * sl);
+        if (nxt < 0) break;
+        unit = nxt;
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // =========================== MMA issuer ===========================
-    if (lane == 0 && nmax > 0) {
+    // =========================== MMA issuer (one thread) ===========================
+    if (lane == 0) {
       constexpr uint32_t FMT = BF16 ? 1u : 0u;
-      // S = Q K^T: A = Q (K-major), B = K (K-major), M=128, N=128
+      // S = Q K^T: A = Q (K-major), B = K (K-major), M=128, N=128; a_negate if scale < 0
       const uint32_t IDESC_QK = make_idesc_f16(FMT, BM, BN, 0, 0, p.neg ? 1u : 0u);
       // O += P V: A = P (K-major), B = V (MN-major: D contiguous), M=128, N=D
       constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, BM, D, 0, 1, 0);
-      mbar_wait(bar_q_full, 0);
-      tc_fence_after();
-      int it = 0;
-      int v_slot_prev = 0, v_use_prev = 0;
-      auto issue_pv = [&](int jj, int vslot, int vuse) {
-        mbar_wait(bar_kv_full(vslot), vuse & 1);
+      int unit = blockIdx.x;
+      int it = 0;                      // K/V ring position (same sequence as the producer)
+      uint32_t cs0 = 0, cs1 = 0;       // S MMAs issued per tile (cumulative)
+      uint32_t cp0 = 0, cp1 = 0;       // PV MMAs issued per tile (cumulative)
+      for (int k = 0;; ++k) {
+        const Unit U = decode_unit(unit, p);
+        const int nmax = max(U.n0, U.n1);
+        mbar_wait(bar_q_full, k & 1);
         tc_fence_after();
+        const int it0 = it;
+        it += 2 * nmax;
+        auto kslot = [&](int j) { return (it0 + 2 * j) % C::NST; };
+        auto kpar = [&](int j) { return ((it0 + 2 * j) / C::NST) & 1; };
+        auto vslot = [&](int j) { return (it0 + 2 * j + 1) % C::NST; };
+        auto vpar = [&](int j) { return ((it0 + 2 * j + 1) / C::NST) & 1; };
+        // S_t(j) = Q_t K_j^T
+        auto issue_s = [&](int t, int j) {
+          uint32_t& cs = t ? cs1 : cs0;
+          mbar_wait(bar_kv_full(kslot(j)), kpar(j));
+          if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // softmax t has read S_t
+          tc_fence_after();
+          const uint32_t tm_s = tmem_base + t * BN;
+          const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
+          const uint32_t kb = sKV + kslot(j) * C::KV_BYTES;
 #pragma unroll
-        for (int t = 0; t < TILES; ++t) {
-          if (jj < n_t[t]) {
-            mbar_wait(bar_p_full(t), jj & 1);
-            tc_fence_after();
-            const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
-            const uint32_t pa = sP + t * C::P_TILE_BYTES;
-            const uint32_t vb = sKV + vslot * C::KV_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-              // A: P rows x 16 keys: key chunk kk/4 (16 KB apart), +32 B per 16 keys
-              const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
-              // B: V 16 keys x D: +16 rows * 128 B per step; LBO = next 64-wide D chunk
-              const uint64_t bd = make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024);
-              mma_f16_ss(tm_o, ad, bd, IDESC_PV, (jj > 0 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(bar_o_done(t));
+          for (int kk = 0; kk < D / 16; ++kk) {
+            // K-major SW128: 16-element K step = +32 B inside the 128-B swizzle row;
+            // every 64 elements the next 16 KB TMA box
+            const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
+            mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
+                       make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
           }
-        }
-        mma_commit(bar_kv_empty(vslot));
-      };
-      for (int j = 0; j < nmax; ++j) {
-        const int k_slot = it % C::NST, k_use = it / C::NST;
-        ++it;
-        const int v_slot = it % C::NST, v_use = it / C::NST;
-        ++it;
-        mbar_wait(bar_kv_full(k_slot), k_use & 1);
-        tc_fence_after();
+          mma_commit(bar_s_full(t));
+          ++cs;
+        };
+        // O_t += P_t V_j
+        auto issue_pv = [&](int t, int j) {
+          uint32_t& cpv = t ? cp1 : cp0;
+          mbar_wait(bar_kv_full(vslot(j)), vpar(j));
+          mbar_wait(bar_p_full(t), cpv & 1);
+          tc_fence_after();
+          const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
+          const uint32_t pa = sP + t * C::P_TILE_BYTES;
+          const uint32_t vb = sKV + vslot(j) * C::KV_BYTES;
 #pragma unroll
-        for (int t = 0; t < TILES; ++t) {
-          if (j < n_t[t]) {
-            if (j > 0) {
-              mbar_wait(bar_s_free(t), (j - 1) & 1);
-              tc_fence_after();
-            }
-            const uint32_t tm_s = tmem_base + t * BN;
-            const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
-            const uint32_t kb = sKV + k_slot * C::KV_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
-              mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
-                         make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
-            }
-            mma_commit(bar_s_full(t));
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            // A = P (K-major SW128, 2 x 16 KB key chunks); B = V MN-major SW128:
+            // 16 keys = 16 rows of 128 B (+2 KB); LBO = 16 KB to the next 64-wide D chunk
+            const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+            const uint64_t bd = make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024);
+            mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
           }
+          mma_commit(bar_o_done(t));
+          ++cpv;
+        };
+        if (nmax > 0) {
+          // Ping-pong order per block j: PV0(j), S0(j+1), PV1(j), S1(j+1): each tile's PV
+          // follows its own P and the other tile's S fills the tensor pipe meanwhile.
+          if (U.n0 > 0) issue_s(0, 0);
+          if (U.n1 > 0) issue_s(1, 0);
+          mma_commit(bar_kv_empty(kslot(0)));
+          if (nmax == 1) mma_commit(bar_q_empty);
+          for (int j = 0; j < nmax; ++j) {
+            const bool more = j + 1 < nmax;
+            if (j < U.n0) issue_pv(0, j);
+            if (j + 1 < U.n0) issue_s(0, j + 1);
+            if (more && j + 1 >= U.n1) {  // tile 1 does not need K_{j+1}
+              mma_commit(bar_kv_empty(kslot(j + 1)));
+              if (j + 2 == nmax) mma_commit(bar_q_empty);
+            }
+            if (j < U.n1) issue_pv(1, j);
+            mma_commit(bar_kv_empty(vslot(j)));
+            if (j + 1 < U.n1) {
+              issue_s(1, j + 1);
+              mma_commit(bar_kv_empty(kslot(j + 1)));
+              if (j + 2 == nmax) mma_commit(bar_q_empty);
+            }
+          }
+        } else {
+          mbar_arrive(bar_q_empty);  // nothing to compute; Q buffer is free again
         }
-        mma_commit(bar_kv_empty(k_slot));
-        if (j > 0) issue_pv(j - 1, v_slot_prev, v_use_prev);
-        v_slot_prev = v_slot;
-        v_use_prev = v_use;
+        mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+        const int nxt = clc_query(sSched + 16 * (k & 1));
+        mbar_arrive(bar_sched_empty(k & 1));
+        if (nxt < 0) break;
+        unit = nxt;
       }
-      issue_pv(nmax - 1, v_slot_prev, v_use_prev);
     }
     __syncwarp();
-  } else if (warp >= SOFTMAX_WARP0) {
+  }
+  } else {
+    setmaxnreg_inc<REGS_SOFTMAX>();
     // =========================== softmax / correction / epilogue ===========================
-    const int t = (warp - SOFTMAX_WARP0) >> 2;     // tile
+    const int t = (warp - SOFTMAX_WARP0) >> 2;     // query tile of the unit
     const int q4 = warp & 3;                        // TMEM lane quarter this warp may access
     const int lr = q4 * 32 + lane;                  // row within tile == TMEM lane
-    const int r0 = m_blk * (TILES * BM) + t * BM;
-    const int row = r0 + lr;                        // global query index
-    const int nt = n_t[t];
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const uint32_t tm_s = tmem_base + lane_off + t * BN;
     const uint32_t tm_o = tmem_base + lane_off + C::TMEM_O + t * D;
     const uint32_t p_row = sP + t * C::P_TILE_BYTES + lr * 128;
     const float c = p.c_log2;
-    // last key index this row may attend to (inclusive)
-    const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
+    int unit = blockIdx.x;
+    uint32_t g = 0;  // blocks processed by this tile's warpgroup (cumulative, barrier phases)
+    for (int k = 0;; ++k) {
+      const Unit U = decode_unit(unit, p);
+      const int nt = t ? U.n1 : U.n0;
+      const int row = U.m_blk * (TILES * BM) + t * BM + lr;  // global query index
+      // last key index this row may attend to (inclusive); bottom-right causal (R3)
+      const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
+      float m = -INFINITY;  // running max of c*s (scores_max; reading R2)
+      float l = 0.f;        // running sum        (logsum)
 
-    float m = -INFINITY;  // running max of c * s   (scores_max; R2)
-    float l = 0.f;        // running sum            (logsum)
-
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait(bar_s_full(t), j & 1);
-      tc_fence_after();
-      float s[BN];
-      {
-        uint32_t* sr = reinterpret_cast<uint32_t*>(s);
+      for (int j = 0; j < nt; ++j, ++g) {
+        mbar_wait(bar_s_full(t), g & 1);
+        tc_fence_after();
+        uint32_t sr[BN];
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc)
           tmem_ld32(tm_s + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + cc * 32));
         tmem_ld_wait();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_s_free(t));  // S_t may be overwritten by the next QK^T
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_s_free(t));  // S_t may be overwritten by QK^T(j+1)
 
-      const int k0 = j * BN;
-      const bool masked = (k0 + BN - 1 > limit);  // any column beyond this row's limit
-      if (__any_sync(0xffffffffu, masked)) {
+        float* s = reinterpret_cast<float*>(sr);
+        const int k0 = j * BN;
+        const bool masked = (k0 + BN - 1 > limit);  // a column beyond this row's last key
+        if (__any_sync(0xffffffffu, masked)) {
 #pragma unroll
-        for (int cc = 0; cc < BN; ++cc)
-          if (k0 + cc > limit) s[cc] = -INFINITY;
-      }
-      // row max (T.reduce_max): in-thread, the thread owns the whole row
-      float mx = s[0];
+          for (int cc = 0; cc < BN; ++cc)
+            if (k0 + cc > limit) s[cc] = -INFINITY;
+        }
+        // row max (T.reduce_max): in-thread, each thread owns one whole S row
+        float mx = s[0];
 #pragma unroll
-      for (int cc = 1; cc < BN; ++cc) mx = fmaxf(mx, s[cc]);
-      const float m_new = fmaxf(m, (mx == -INFINITY) ? -INFINITY : mx * c);
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
-      const float alpha = ex2(m - m_use);                      // scores_scale
-      // p = exp2(s*c - m), row sum from unrounded fp32 p (R8)
-      float sum = 0.f;
-      uint32_t pk[BN / 2];
+        for (int cc = 1; cc < BN; ++cc) mx = fmaxf(mx, s[cc]);
+        const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
+        const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
+        const float alpha = ex2(m - m_use);                      // scores_scale
+        // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8)
+        float sum = 0.f;
+        uint32_t pk[BN / 2];
 #pragma unroll
-      for (int cc = 0; cc < BN; cc += 2) {
-        float p0 = ex2(fmaf(s[cc], c, -m_use));
-        float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
-        if (s[cc] == -INFINITY) p0 = 0.f;
-        if (s[cc + 1] == -INFINITY) p1 = 0.f;
-        sum += p0 + p1;
-        pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype
-      }
-      if (j > 0) {
-        // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
-        mbar_wait(bar_o_done(t), (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // acc_o *= scores_scale
+        for (int cc = 0; cc < BN; cc += 2) {
+          float p0 = ex2(fmaf(s[cc], c, -m_use));
+          float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
+          if (s[cc] == -INFINITY) p0 = 0.f;
+          if (s[cc + 1] == -INFINITY) p1 = 0.f;
+          sum += p0 + p1;
+          pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+        }
+        if (j > 0) {
+          // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
+          mbar_wait(bar_o_done(t), (g - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {  // acc_o *= scores_scale
 #pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t ov[32];
-            tmem_ld32(tm_o + cc * 32, ov);
-            tmem_ld_wait();
+            for (int cc = 0; cc < D / 32; ++cc) {
+              uint32_t ov[32];
+              tmem_ld32(tm_o + cc * 32, ov);
+              tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st32(tm_o + cc * 32, ov);
+              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st32(tm_o + cc * 32, ov);
+            }
+            tmem_st_wait();
           }
-          tmem_st_wait();
         }
-      }
-      // P row -> smem, K-major SWIZZLE_128B: 16-B unit u of 64-key chunk goes to u ^ (row & 7)
+        // P row -> smem, K-major SWIZZLE_128B: 16-B unit u of a 64-key chunk -> u ^ (row & 7)
 #pragma unroll
-      for (int ch = 0; ch < BN / 64; ++ch) {
+        for (int ch = 0; ch < BN / 64; ++ch) {
 #pragma unroll
-        for (int uu = 0; uu < 8; ++uu) {
-          const uint32_t addr = p_row + ch * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
-          const int w = ch * 32 + uu * 4;
-          st_shared_v4(addr, pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
+          for (int uu = 0; uu < 8; ++uu) {
+            const uint32_t addr = p_row + ch * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
+            const int w = ch * 32 + uu * 4;
+            st_shared_v4(addr, pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
+          }
         }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_p_full(t));
+        l = l * alpha + sum;  // logsum = logsum * scores_scale + scores_sum
+        m = m_new;
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_p_full(t));
-      l = l * alpha + sum;  // logsum = logsum * scores_scale + scores_sum
-      m = m_new;
-    }
 
-    // ---- epilogue: O / l, LSE, store
-    if (nt > 0) {
-      mbar_wait(bar_o_done(t), (nt - 1) & 1);
-      tc_fence_after();
-    }
-    const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
-    const bool row_ok = row < p.Sq;
-    uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
-                    ((((size_t)b * p.Sq + (row_ok ? row : 0)) * p.Hq + h) * D) * 2;
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t ov[32];
+      // ---- epilogue: O / l, LSE, store
       if (nt > 0) {
-        tmem_ld32(tm_o + cc * 32, ov);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ov[e] = 0u;
+        mbar_wait(bar_o_done(t), (g - 1) & 1);
+        tc_fence_after();
       }
-      uint32_t pkd[16];
+      const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
+      const bool row_ok = row < p.Sq;
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
+                      ((((size_t)U.b * p.Sq + (row_ok ? row : 0)) * p.Hq + U.h) * D) * 2;
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
-        pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
-      if (row_ok) {
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t ov[32];
+        if (nt > 0) {
+          tmem_ld32(tm_o + cc * 32, ov);
+          tmem_ld_wait();
+        } else {
 #pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4)
-          st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2], pkd[4 * v4 + 3]);
+          for (int e = 0; e < 32; ++e) ov[e] = 0u;
+        }
+        uint32_t pkd[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
+        if (row_ok) {
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4)
+            st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2],
+                         pkd[4 * v4 + 3]);
+        }
       }
+      if (p.lse != nullptr && row_ok) {
+        // lse = ln sum exp(scale*s) = (m + log2 l) ln 2, m in log2 units (reading R5)
+        p.lse[((size_t)U.b * p.Hq + U.h) * p.Sq + row] =
+            (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+      }
+      tc_fence_before();  // O_t reads complete before the next unit's first PV_t overwrites
+
+      mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+      const int nxt = clc_query(sSched + 16 * (k & 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_sched_empty(k & 1));
+      if (nxt < 0) break;
+      unit = nxt;
     }
-    if (p.lse != nullptr && row_ok) {
-      // lse = ln(sum exp(scale*s)) = (m + log2 l) * ln 2 with m in log2 units
-      p.lse[((size_t)b * p.Hq + h) * p.Sq + row] =
-          (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-    }
-    tc_fence_before();
   }
 
   __syncthreads();

@@ -220,6 +220,45 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// ------------------------------------------------------------------ cluster launch control
+// Hardware work stealing (sm_100): cancel a not-yet-launched CTA of this grid and take
+// its work. The 16-byte response lands in smem and completes `bar`'s transaction count.
+__device__ __forceinline__ void clc_try_cancel(uint32_t resp_smem, uint32_t bar) {
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 "
+      "[%0], [%1];" ::"r"(resp_smem),
+      "r"(bar)
+      : "memory");
+}
+
+// Decode a response: returns the stolen CTA's blockIdx.x, or -1 if nothing was canceled.
+__device__ __forceinline__ int clc_query(uint32_t resp_smem) {
+  uint64_t lo, hi;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(resp_smem) : "memory");
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 rr;\n\t.reg .pred p;\n\t"
+      "mov.b128 rr, {%2, %3};\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, rr;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "mov.u32 %1, 0;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, rr;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "l"(lo), "l"(hi));
+  return ok ? static_cast<int>(x) : -1;
+}
+
+// ------------------------------------------------------------------ register rebalancing
+// Per-warpgroup register budget (all 4 warps of the warpgroup must execute it).
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ------------------------------------------------------------------ misc math
 __device__ __forceinline__ float ex2(float x) {
   float y;
