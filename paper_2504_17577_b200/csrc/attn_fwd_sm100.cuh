@@ -7,9 +7,9 @@
 //         Q_shared / acc_s / acc_o; here M=128 per tcgen05 tile]
 //   warp 0        TMA producer: Q tiles once (T.copy Q), then K_j, V_j into an
 //                 NST-slot mbarrier ring (T.Pipelined num_stages)
-//   warp 1        MMA issuer (one thread): S_t = Q_t K_j^T (T.gemm transpose_B)
-//                 and O_t += P_t V_j (T.gemm) with tcgen05.mma, accumulators
-//                 in TMEM; tcgen05.commit -> mbarriers
+//   warps 1, 2    MMA issuers (one thread each, one per query tile t): S_t = Q_t K_j^T
+//                 (T.gemm transpose_B) and O_t += P_t V_j (T.gemm) with
+//                 tcgen05.mma, accumulators in TMEM; tcgen05.commit -> mbarriers
 //   warps 4-7     softmax for tile 0, warps 8-11 softmax for tile 1: tcgen05.ld of the
 //                 S row (one thread owns one row: TMEM lane = row), mask, running max,
 //                 exp2, row sum, O rescale in TMEM, P -> smem
@@ -157,10 +157,10 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     prefetch_tmap(&p.tm_k);
     prefetch_tmap(&p.tm_v);
     mbar_init(bar_q_full, 1);
-    mbar_init(bar_q_empty, 1);
+    mbar_init(bar_q_empty, 2);  // one release per MMA issuer
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(bar_kv_full(s), 1);
-      mbar_init(bar_kv_empty(s), 1);
+      mbar_init(bar_kv_empty(s), 2);  // one release per MMA issuer
     }
     for (int t = 0; t < TILES; ++t) {
       mbar_init(bar_s_full(t), 1);
@@ -170,7 +170,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_sched_full(i), 1);
-      mbar_init(bar_sched_empty(i), 1 + 8);  // MMA thread + 8 softmax warps
+      mbar_init(bar_sched_empty(i), 2 + 8);  // 2 MMA issuers + 8 softmax warps
     }
     fence_mbar_init();
   }
@@ -236,57 +236,62 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    // =========================== MMA issuer (one thread) ===========================
+  } else if (warp == 1 || warp == 2) {
+    // ==================== MMA issuers: warp 1 -> tile 0, warp 2 -> tile 1 ====================
+    // One issuing thread per query tile, each with blocking waits in its tile's natural
+    // event order: S_t(j+1) as soon as softmax t has read S_t(j) (P lives in smem, so the
+    // S buffer frees early), then PV_t(j) once P_t(j) is written. The tensor pipe
+    // interleaves the two streams. K/V slots, the Q buffer and the scheduler slot are
+    // released by BOTH issuers (barrier counts 2).
+    const int t = warp - 1;
     if (lane == 0) {
       constexpr uint32_t FMT = BF16 ? 1u : 0u;
       // S = Q K^T: A = Q (K-major), B = K (K-major), M=128, N=128; a_negate if scale < 0
       const uint32_t IDESC_QK = make_idesc_f16(FMT, BM, BN, 0, 0, p.neg ? 1u : 0u);
       // O += P V: A = P (K-major), B = V (MN-major: D contiguous), M=128, N=D
       constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, BM, D, 0, 1, 0);
+      const uint32_t tm_s = tmem_base + t * BN;
+      const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
+      const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
+      const uint32_t pa = sP + t * C::P_TILE_BYTES;
       int unit = blockIdx.x;
-      int it = 0;                      // K/V ring position (same sequence as the producer)
-      uint32_t cs0 = 0, cs1 = 0;       // S MMAs issued per tile (cumulative)
-      uint32_t cp0 = 0, cp1 = 0;       // PV MMAs issued per tile (cumulative)
+      int it = 0;        // K/V ring position (same sequence as the producer)
+      uint32_t cs = 0;   // S MMAs issued by this tile (cumulative: barrier phases)
+      uint32_t cpv = 0;  // PV MMAs issued by this tile
       for (int k = 0;; ++k) {
         const Unit U = decode_unit(unit, p);
         const int nmax = max(U.n0, U.n1);
-        mbar_wait(bar_q_full, k & 1);
-        tc_fence_after();
+        const int nt = t ? U.n1 : U.n0;
         const int it0 = it;
         it += 2 * nmax;
         auto kslot = [&](int j) { return (it0 + 2 * j) % C::NST; };
         auto kpar = [&](int j) { return ((it0 + 2 * j) / C::NST) & 1; };
         auto vslot = [&](int j) { return (it0 + 2 * j + 1) % C::NST; };
         auto vpar = [&](int j) { return ((it0 + 2 * j + 1) / C::NST) & 1; };
+        mbar_wait(bar_q_full, k & 1);
         // S_t(j) = Q_t K_j^T
-        auto issue_s = [&](int t, int j) {
-          uint32_t& cs = t ? cs1 : cs0;
+        auto issue_s = [&](int j) {
           mbar_wait(bar_kv_full(kslot(j)), kpar(j));
           if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // softmax t has read S_t
           tc_fence_after();
-          const uint32_t tm_s = tmem_base + t * BN;
-          const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
           const uint32_t kb = sKV + kslot(j) * C::KV_BYTES;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            // K-major SW128: 16-element K step = +32 B inside the 128-B swizzle row;
+            // K-major SW128: a 16-element K step is +32 B inside the 128-B swizzle row;
             // every 64 elements the next 16 KB TMA box
             const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
             mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
                        make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
           }
           mma_commit(bar_s_full(t));
+          mma_commit(bar_kv_empty(kslot(j)));  // this tile is done with K_j
           ++cs;
         };
         // O_t += P_t V_j
-        auto issue_pv = [&](int t, int j) {
-          uint32_t& cpv = t ? cp1 : cp0;
+        auto issue_pv = [&](int j) {
           mbar_wait(bar_kv_full(vslot(j)), vpar(j));
           mbar_wait(bar_p_full(t), cpv & 1);
           tc_fence_after();
-          const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
-          const uint32_t pa = sP + t * C::P_TILE_BYTES;
           const uint32_t vb = sKV + vslot(j) * C::KV_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
@@ -297,33 +302,29 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
             mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(bar_o_done(t));
+          mma_commit(bar_kv_empty(vslot(j)));  // this tile is done with V_j
           ++cpv;
         };
-        if (nmax > 0) {
-          // Ping-pong order per block j: PV0(j), S0(j+1), PV1(j), S1(j+1): each tile's PV
-          // follows its own P and the other tile's S fills the tensor pipe meanwhile.
-          if (U.n0 > 0) issue_s(0, 0);
-          if (U.n1 > 0) issue_s(1, 0);
-          mma_commit(bar_kv_empty(kslot(0)));
-          if (nmax == 1) mma_commit(bar_q_empty);
-          for (int j = 0; j < nmax; ++j) {
-            const bool more = j + 1 < nmax;
-            if (j < U.n0) issue_pv(0, j);
-            if (j + 1 < U.n0) issue_s(0, j + 1);
-            if (more && j + 1 >= U.n1) {  // tile 1 does not need K_{j+1}
-              mma_commit(bar_kv_empty(kslot(j + 1)));
-              if (j + 2 == nmax) mma_commit(bar_q_empty);
+        if (nt > 0) {
+          issue_s(0);
+          if (nt == 1) mma_commit(bar_q_empty);
+          for (int j = 0; j < nt; ++j) {
+            if (j + 1 < nt) {
+              issue_s(j + 1);
+              if (j + 2 == nt) mma_commit(bar_q_empty);  // last QK^T of this tile issued
             }
-            if (j < U.n1) issue_pv(1, j);
-            mma_commit(bar_kv_empty(vslot(j)));
-            if (j + 1 < U.n1) {
-              issue_s(1, j + 1);
-              mma_commit(bar_kv_empty(kslot(j + 1)));
-              if (j + 2 == nmax) mma_commit(bar_q_empty);
-            }
+            issue_pv(j);
           }
         } else {
-          mbar_arrive(bar_q_empty);  // nothing to compute; Q buffer is free again
+          mbar_arrive(bar_q_empty);
+        }
+        // blocks this tile skips (causal): release its share of their K/V slots, after the
+        // slot holds that block (so the arrival counts toward the right phase)
+        for (int j = nt; j < nmax; ++j) {
+          mbar_wait(bar_kv_full(kslot(j)), kpar(j));
+          mbar_arrive(bar_kv_empty(kslot(j)));
+          mbar_wait(bar_kv_full(vslot(j)), vpar(j));
+          mbar_arrive(bar_kv_empty(vslot(j)));
         }
         mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
         const int nxt = clc_query(sSched + 16 * (k & 1));
@@ -370,32 +371,53 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
 
         float* s = reinterpret_cast<float*>(sr);
         const int k0 = j * BN;
-        const bool masked = (k0 + BN - 1 > limit);  // a column beyond this row's last key
-        if (__any_sync(0xffffffffu, masked)) {
+        // any column beyond this row's last key? (diagonal / tail blocks only)
+        const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
+        if (masked) {
 #pragma unroll
           for (int cc = 0; cc < BN; ++cc)
             if (k0 + cc > limit) s[cc] = -INFINITY;
         }
         // row max (T.reduce_max): in-thread, each thread owns one whole S row
-        float mx = s[0];
+        float mq[4];
 #pragma unroll
-        for (int cc = 1; cc < BN; ++cc) mx = fmaxf(mx, s[cc]);
+        for (int r = 0; r < 4; ++r) mq[r] = fmax3(s[r * 32], s[r * 32 + 1], s[r * 32 + 2]);
+#pragma unroll
+        for (int cc = 3; cc + 1 < 32; cc += 2)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) mq[r] = fmax3(mq[r], s[r * 32 + cc], s[r * 32 + cc + 1]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mq[r] = fmaxf(mq[r], s[r * 32 + 31]);
+        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
         const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
         const float alpha = ex2(m - m_use);                      // scores_scale
         // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8)
-        float sum = 0.f;
+        float sum0 = 0.f, sum1 = 0.f;
         uint32_t pk[BN / 2];
+        if (masked) {
 #pragma unroll
-        for (int cc = 0; cc < BN; cc += 2) {
-          float p0 = ex2(fmaf(s[cc], c, -m_use));
-          float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
-          if (s[cc] == -INFINITY) p0 = 0.f;
-          if (s[cc + 1] == -INFINITY) p1 = 0.f;
-          sum += p0 + p1;
-          pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+          for (int cc = 0; cc < BN; cc += 2) {
+            float p0 = ex2(fmaf(s[cc], c, -m_use));
+            float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
+            if (s[cc] == -INFINITY) p0 = 0.f;
+            if (s[cc + 1] == -INFINITY) p1 = 0.f;
+            sum0 += p0;
+            sum1 += p1;
+            pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < BN; cc += 2) {
+            const float p0 = ex2(fmaf(s[cc], c, -m_use));
+            const float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
+            sum0 += p0;
+            sum1 += p1;
+            pk[cc / 2] = pack2<BF16>(p0, p1);
+          }
         }
+        const float sum = sum0 + sum1;
         if (j > 0) {
           // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
           mbar_wait(bar_o_done(t), (g - 1) & 1);
