@@ -55,8 +55,13 @@ template <int D>
 struct KCfg {
   static constexpr int Q_TILE_BYTES = BM * D * 2;
   static constexpr int KV_BYTES = BN * D * 2;
+#ifdef TLATTN_NST_OVERRIDE  // experiments only (P smem dropped)
+  static constexpr int NST = TLATTN_NST_OVERRIDE;
+  static constexpr int P_TILE_BYTES = 0;
+#else
   static constexpr int NST = (D == 128) ? 3 : 6;
   static constexpr int P_TILE_BYTES = BM * BN * 2;
+#endif
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + TILES * Q_TILE_BYTES;
   static constexpr int OFF_P = OFF_KV + NST * KV_BYTES;
@@ -101,6 +106,50 @@ __device__ __forceinline__ int tile_nblocks(int r0, const AttnParams& p) {
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr uint32_t REGS_SMALL = 88;     // warpgroup 0: 128 x 88
 constexpr uint32_t REGS_SOFTMAX = 208;  // warpgroups 1-2: 256 x 208 (total 64512 <= 64K)
+
+// exp2 on the FMA pipe for a pair of values: round-to-nearest
+// range reduction with the 1.5*2^23 magic add, 2^f on f in [-0.5, 0.5] by a degree-3
+// polynomial with p(0) = 1 (max relative error 1.0e-4, fitted in tools/fit_exp2_poly.py),
+// and the integer part added to the exponent field with one integer multiply-add.
+// Inputs are clamped to >= -125 so the exponent never underflows (2^-125 contributes
+// nothing visible next to the row max's p >= 1).
+struct Exp2Poly {
+  uint64_t magic, neg_magic, neg_one, c3, c2, c1, one;
+  __device__ __forceinline__ Exp2Poly()
+      : magic(f2pack(12582912.f, 12582912.f)),
+        neg_magic(f2pack(-12582912.f, -12582912.f)),
+        neg_one(f2pack(-1.f, -1.f)),
+        c3(f2pack(0.055008258670568466f, 0.055008258670568466f)),
+        c2(f2pack(0.24220958352088928f, 0.24220958352088928f)),
+        c1(f2pack(0.6932828426361084f, 0.6932828426361084f)),
+        one(f2pack(1.f, 1.f)) {}
+  __device__ __forceinline__ void operator()(uint64_t x2, float& y0, float& y1) const {
+    float x0, x1;
+    f2unpack(x2, x0, x1);
+    x2 = f2pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+    const uint64_t t = fadd2(x2, magic);          // RN(x) in the low mantissa bits
+    const uint64_t f = ffma2(fadd2(t, neg_magic), neg_one, x2);  // x - RN(x) in [-0.5, 0.5]
+    const uint64_t pp = ffma2(ffma2(ffma2(c3, f, c2), f, c1), f, one);
+    float t0, t1, p0, p1;
+    f2unpack(t, t0, t1);
+    f2unpack(pp, p0, p1);
+    // 2^RN(x) * p: add RN(x) to the exponent field (t's low bits hold RN(x) mod 2^9)
+    y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+  }
+};
+
+// Column pairs (of 64 per row) whose exp2 runs on the FMA pipe instead of MUFU.
+// TLATTN_EXP_VARIANT (experiments only): 0 = 3/8 emulated (default), 1 = none emulated,
+// 2 = all emulated, 3 = no exp at all (timing of everything else; WRONG results).
+#ifndef TLATTN_EXP_VARIANT
+#define TLATTN_EXP_VARIANT 0
+#endif
+__host__ __device__ constexpr bool emu_pair(int q) {
+  return TLATTN_EXP_VARIANT == 2 ? true
+       : TLATTN_EXP_VARIANT == 1 ? false
+       : ((q & 7) == 2 || (q & 7) == 5 || (q & 7) == 7);
+}
 
 struct Unit {
   int b, h, hkv, m_blk, n0, n1;
@@ -216,18 +265,19 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
                           U.h, r00 + t * BM, U.b, pol_q);
           }
         }
-        for (int j = 0; j < nmax; ++j) {
+        // Load order = MMA consumption order: K_0, then K_{j+1} before V_j, so the next
+        // QK^T's operand is never queued behind a V tile that waits for softmax(j).
+        for (int q = 0; q < 2 * nmax; ++q, ++it) {
+          const bool is_k = (q == 0) || ((q & 1) && q != 2 * nmax - 1);
+          const int j = (q == 0) ? 0 : (is_k ? (q + 1) >> 1 : (q == 2 * nmax - 1 ? nmax - 1 : (q - 2) >> 1));
+          const int slot = it % C::NST;
+          const int use = it / C::NST;
+          if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
+          mbar_arrive_expect_tx(bar_kv_full(slot), C::KV_BYTES);
 #pragma unroll
-          for (int kv = 0; kv < 2; ++kv, ++it) {
-            const int slot = it % C::NST;
-            const int use = it / C::NST;
-            if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
-            mbar_arrive_expect_tx(bar_kv_full(slot), C::KV_BYTES);
-#pragma unroll
-            for (int c = 0; c < D / 64; ++c)
-              tma_load_4d(sKV + slot * C::KV_BYTES + c * CHUNK_BYTES, kv == 0 ? &p.tm_k : &p.tm_v,
-                          bar_kv_full(slot), c * 64, U.hkv, j * BN, U.b, pol_kv);
-          }
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_4d(sKV + slot * C::KV_BYTES + c * CHUNK_BYTES, is_k ? &p.tm_k : &p.tm_v,
+                        bar_kv_full(slot), c * 64, U.hkv, j * BN, U.b, pol_kv);
         }
         mbar_wait(bar_sched_full(sl), (k >> 1) & 1);
         const int nxt = clc_query(sSched + 16 * sl);
@@ -264,19 +314,27 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         const int nt = t ? U.n1 : U.n0;
         const int it0 = it;
         it += 2 * nmax;
-        auto kslot = [&](int j) { return (it0 + 2 * j) % C::NST; };
-        auto kpar = [&](int j) { return ((it0 + 2 * j) / C::NST) & 1; };
-        auto vslot = [&](int j) { return (it0 + 2 * j + 1) % C::NST; };
-        auto vpar = [&](int j) { return ((it0 + 2 * j + 1) / C::NST) & 1; };
+        // ring positions (producer order K_0, K_1, V_0, K_2, V_1, ..., V_{nmax-1})
+        auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
+        auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
+        auto kslot = [&](int j) { return kpos(j) % C::NST; };
+        auto kpar = [&](int j) { return (kpos(j) / C::NST) & 1; };
+        auto vslot = [&](int j) { return vpos(j) % C::NST; };
+        auto vpar = [&](int j) { return (vpos(j) / C::NST) & 1; };
         mbar_wait(bar_q_full, k & 1);
         // S_t(j) = Q_t K_j^T
         auto issue_s = [&](int j) {
           mbar_wait(bar_kv_full(kslot(j)), kpar(j));
+#ifndef TLATTN_MMA_ONLY
           if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // softmax t has read S_t
+#endif
           tc_fence_after();
           const uint32_t kb = sKV + kslot(j) * C::KV_BYTES;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
+#ifdef TLATTN_SKIP_S
+            break;
+#endif
             // K-major SW128: a 16-element K step is +32 B inside the 128-B swizzle row;
             // every 64 elements the next 16 KB TMA box
             const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
@@ -290,11 +348,16 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         // O_t += P_t V_j
         auto issue_pv = [&](int j) {
           mbar_wait(bar_kv_full(vslot(j)), vpar(j));
+#ifndef TLATTN_MMA_ONLY
           mbar_wait(bar_p_full(t), cpv & 1);
+#endif
           tc_fence_after();
           const uint32_t vb = sKV + vslot(j) * C::KV_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
+#ifdef TLATTN_SKIP_PV
+            break;
+#endif
             // A = P (K-major SW128, 2 x 16 KB key chunks); B = V MN-major SW128:
             // 16 keys = 16 rows of 128 B (+2 KB); LBO = 16 KB to the next 64-wide D chunk
             const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
@@ -350,7 +413,11 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     uint32_t g = 0;  // blocks processed by this tile's warpgroup (cumulative, barrier phases)
     for (int k = 0;; ++k) {
       const Unit U = decode_unit(unit, p);
+#ifdef TLATTN_MMA_ONLY
+      const int nt = 0;  // experiment: tensor/TMA data path alone
+#else
       const int nt = t ? U.n1 : U.n0;
+#endif
       const int row = U.m_blk * (TILES * BM) + t * BM + lr;  // global query index
       // last key index this row may attend to (inclusive); bottom-right causal (R3)
       const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
@@ -408,14 +475,35 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
             pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
           }
         } else {
+          // unmasked block: paired FFMA2 for s*c - m, FADD2 row sums; 3 of every 8 column
+          // pairs take exp2 on the FMA pipe (Exp2Poly), the rest on MUFU
+          const uint64_t c2 = f2pack(c, c);
+          const uint64_t nm2 = f2pack(-m_use, -m_use);
+          const Exp2Poly poly;
+          uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-          for (int cc = 0; cc < BN; cc += 2) {
-            const float p0 = ex2(fmaf(s[cc], c, -m_use));
-            const float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
-            sum0 += p0;
-            sum1 += p1;
-            pk[cc / 2] = pack2<BF16>(p0, p1);
+          for (int q = 0; q < BN / 2; ++q) {
+            const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
+            float p0, p1;
+            if (TLATTN_EXP_VARIANT == 3) {
+              f2unpack(x2, p0, p1);
+            } else if (emu_pair(q)) {
+              poly(x2, p0, p1);
+            } else {
+              float x0, x1;
+              f2unpack(x2, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
+            else acc0 = fadd2(acc0, f2pack(p0, p1));
+            pk[q] = pack2<BF16>(p0, p1);
           }
+          float a0, a1, b0, b1;
+          f2unpack(acc0, a0, a1);
+          f2unpack(acc1, b0, b1);
+          sum0 = a0 + b0;
+          sum1 = a1 + b1;
         }
         const float sum = sum0 + sum1;
         if (j > 0) {
@@ -440,6 +528,9 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         for (int ch = 0; ch < BN / 64; ++ch) {
 #pragma unroll
           for (int uu = 0; uu < 8; ++uu) {
+#ifdef TLATTN_NO_PSTORE
+            if (uu != 0) continue;
+#endif
             const uint32_t addr = p_row + ch * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
             const int w = ch * 32 + uu * 4;
             st_shared_v4(addr, pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);

@@ -36,7 +36,7 @@ def load_library(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or LIB
+        path = path or os.environ.get("TLATTN_LIB") or LIB
         if not os.path.exists(path):
             raise RuntimeError(f"libtlattn.so not found at {path}: run __graft_entry__.build() "
                                "(there is no CPU fallback)")
