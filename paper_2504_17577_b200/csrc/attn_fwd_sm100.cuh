@@ -139,16 +139,103 @@ struct Exp2Poly {
   }
 };
 
-// Column pairs (of 64 per row) whose exp2 runs on the FMA pipe instead of MUFU.
-// TLATTN_EXP_VARIANT (experiments only): 0 = 3/8 emulated (default), 1 = none emulated,
-// 2 = all emulated, 3 = no exp at all (timing of everything else; WRONG results).
+// Column pairs (of 64 per row) whose exp2 runs on the FMA pipe instead of MUFU: EMU of
+// every 8. Measured on B200: D=64 gains from EMU=3 (the softmax
+// bounds that shape), D=128 is fastest with EMU=0 (the extra issue slots cost more than
+// the MUFU time saved).
+// TLATTN_EXP_VARIANT (experiments only): 0 = per-kernel EMU, 1 = none, 2 = all,
+// 3 = no exp at all (timing of everything else; WRONG results).
 #ifndef TLATTN_EXP_VARIANT
 #define TLATTN_EXP_VARIANT 0
 #endif
+template <int EMU>
 __host__ __device__ constexpr bool emu_pair(int q) {
   return TLATTN_EXP_VARIANT == 2 ? true
        : TLATTN_EXP_VARIANT == 1 ? false
-       : ((q & 7) == 2 || (q & 7) == 5 || (q & 7) == 7);
+       : EMU == 3 ? ((q & 7) == 2 || (q & 7) == 5 || (q & 7) == 7)
+       : EMU == 2 ? ((q & 7) == 3 || (q & 7) == 7)
+       : EMU == 1 ? ((q & 7) == 7)
+       : false;
+}
+
+
+// One K/V block of the online softmax for the row this thread owns (Fig. 18
+// P:L660-679): mask (diagonal / tail blocks only), row max, conditional running-max
+// update, p = exp2(s*c - m) with part of the exp2s on the FMA pipe, fp32 row sum of the
+// unrounded p, and P packed (RN) to the input dtype. sr[] holds the raw fp32 S row.
+template <bool BF16, int EMU>
+__device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, int limit, float c,
+                                                  float m, float& m_new_out, float& alpha_out,
+                                                  float& sum_out, uint32_t (&pk)[BN / 2]) {
+  float* s = reinterpret_cast<float*>(sr);
+  // any column beyond this row's last key? (diagonal / tail blocks only)
+  const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
+  if (masked) {
+#pragma unroll
+    for (int cc = 0; cc < BN; ++cc)
+      if (k0 + cc > limit) s[cc] = -INFINITY;
+  }
+  // row max (T.reduce_max): in-thread, each thread owns one whole S row
+  float mq[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) mq[r] = fmax3(s[r * 32], s[r * 32 + 1], s[r * 32 + 2]);
+#pragma unroll
+  for (int cc = 3; cc + 1 < 32; cc += 2)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) mq[r] = fmax3(mq[r], s[r * 32 + cc], s[r * 32 + cc + 1]);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) mq[r] = fmaxf(mq[r], s[r * 32 + 31]);
+  const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+  const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
+  const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
+  const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
+  alpha_out = ex2(m - m_use);                              // scores_scale
+  m_new_out = m_new;
+  // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8)
+  float sum0 = 0.f, sum1 = 0.f;
+  if (masked) {
+#pragma unroll
+    for (int cc = 0; cc < BN; cc += 2) {
+      float p0 = ex2(fmaf(s[cc], c, -m_use));
+      float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
+      if (s[cc] == -INFINITY) p0 = 0.f;
+      if (s[cc + 1] == -INFINITY) p1 = 0.f;
+      sum0 += p0;
+      sum1 += p1;
+      pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+    }
+  } else {
+    // unmasked block: paired FFMA2 for s*c - m, FADD2 row sums; emu_pair() column pairs
+    // take exp2 on the FMA pipe (Exp2Poly), the rest on MUFU
+    const uint64_t c2 = f2pack(c, c);
+    const uint64_t nm2 = f2pack(-m_use, -m_use);
+    const Exp2Poly poly;
+    uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+    for (int q = 0; q < BN / 2; ++q) {
+      const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
+      float p0, p1;
+      if (TLATTN_EXP_VARIANT == 3) {
+        f2unpack(x2, p0, p1);
+      } else if (emu_pair<EMU>(q)) {
+        poly(x2, p0, p1);
+      } else {
+        float x0, x1;
+        f2unpack(x2, x0, x1);
+        p0 = ex2(x0);
+        p1 = ex2(x1);
+      }
+      if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
+      else acc0 = fadd2(acc0, f2pack(p0, p1));
+      pk[q] = pack2<BF16>(p0, p1);
+    }
+    float a0, a1, b0, b1;
+    f2unpack(acc0, a0, a1);
+    f2unpack(acc1, b0, b1);
+    sum0 = a0 + b0;
+    sum1 = a1 + b1;
+  }
+  sum_out = sum0 + sum1;
 }
 
 struct Unit {
@@ -175,6 +262,9 @@ template <int D, bool BF16>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
   using C = KCfg<D>;
+  // K/V load order: D=128 loads K_{j+1} ahead of V_j (MMA consumption order, measured
+  // faster with the 3-slot ring); D=64 has a 6-slot ring and keeps K_j, V_j pairs.
+  constexpr bool K_AHEAD = (D == 128);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;  // 1024-B aligned (SWIZZLE_128B atoms)
@@ -268,8 +358,15 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         // Load order = MMA consumption order: K_0, then K_{j+1} before V_j, so the next
         // QK^T's operand is never queued behind a V tile that waits for softmax(j).
         for (int q = 0; q < 2 * nmax; ++q, ++it) {
-          const bool is_k = (q == 0) || ((q & 1) && q != 2 * nmax - 1);
-          const int j = (q == 0) ? 0 : (is_k ? (q + 1) >> 1 : (q == 2 * nmax - 1 ? nmax - 1 : (q - 2) >> 1));
+          bool is_k;
+          int j;
+          if (K_AHEAD) {
+            is_k = (q == 0) || ((q & 1) && q != 2 * nmax - 1);
+            j = (q == 0) ? 0 : (is_k ? (q + 1) >> 1 : (q == 2 * nmax - 1 ? nmax - 1 : (q - 2) >> 1));
+          } else {
+            is_k = (q & 1) == 0;
+            j = q >> 1;
+          }
           const int slot = it % C::NST;
           const int use = it / C::NST;
           if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
@@ -315,8 +412,10 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         const int it0 = it;
         it += 2 * nmax;
         // ring positions (producer order K_0, K_1, V_0, K_2, V_1, ..., V_{nmax-1})
-        auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
-        auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
+        auto kpos = [&](int j) { return it0 + (K_AHEAD ? (j == 0 ? 0 : 2 * j - 1) : 2 * j); };
+        auto vpos = [&](int j) {
+          return it0 + (K_AHEAD ? (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2) : 2 * j + 1);
+        };
         auto kslot = [&](int j) { return kpos(j) % C::NST; };
         auto kpar = [&](int j) { return (kpos(j) / C::NST) & 1; };
         auto vslot = [&](int j) { return vpos(j) % C::NST; };
@@ -436,76 +535,9 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s_free(t));  // S_t may be overwritten by QK^T(j+1)
 
-        float* s = reinterpret_cast<float*>(sr);
-        const int k0 = j * BN;
-        // any column beyond this row's last key? (diagonal / tail blocks only)
-        const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
-        if (masked) {
-#pragma unroll
-          for (int cc = 0; cc < BN; ++cc)
-            if (k0 + cc > limit) s[cc] = -INFINITY;
-        }
-        // row max (T.reduce_max): in-thread, each thread owns one whole S row
-        float mq[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) mq[r] = fmax3(s[r * 32], s[r * 32 + 1], s[r * 32 + 2]);
-#pragma unroll
-        for (int cc = 3; cc + 1 < 32; cc += 2)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) mq[r] = fmax3(mq[r], s[r * 32 + cc], s[r * 32 + cc + 1]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) mq[r] = fmaxf(mq[r], s[r * 32 + 31]);
-        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
-        const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
-        const float alpha = ex2(m - m_use);                      // scores_scale
-        // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8)
-        float sum0 = 0.f, sum1 = 0.f;
+        float m_new, alpha, sum;
         uint32_t pk[BN / 2];
-        if (masked) {
-#pragma unroll
-          for (int cc = 0; cc < BN; cc += 2) {
-            float p0 = ex2(fmaf(s[cc], c, -m_use));
-            float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
-            if (s[cc] == -INFINITY) p0 = 0.f;
-            if (s[cc + 1] == -INFINITY) p1 = 0.f;
-            sum0 += p0;
-            sum1 += p1;
-            pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
-          }
-        } else {
-          // unmasked block: paired FFMA2 for s*c - m, FADD2 row sums; 3 of every 8 column
-          // pairs take exp2 on the FMA pipe (Exp2Poly), the rest on MUFU
-          const uint64_t c2 = f2pack(c, c);
-          const uint64_t nm2 = f2pack(-m_use, -m_use);
-          const Exp2Poly poly;
-          uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
-#pragma unroll
-          for (int q = 0; q < BN / 2; ++q) {
-            const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
-            float p0, p1;
-            if (TLATTN_EXP_VARIANT == 3) {
-              f2unpack(x2, p0, p1);
-            } else if (emu_pair(q)) {
-              poly(x2, p0, p1);
-            } else {
-              float x0, x1;
-              f2unpack(x2, x0, x1);
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-            }
-            if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
-            else acc0 = fadd2(acc0, f2pack(p0, p1));
-            pk[q] = pack2<BF16>(p0, p1);
-          }
-          float a0, a1, b0, b1;
-          f2unpack(acc0, a0, a1);
-          f2unpack(acc1, b0, b1);
-          sum0 = a0 + b0;
-          sum1 = a1 + b1;
-        }
-        const float sum = sum0 + sum1;
+        softmax_row_block<BF16, (D == 64 ? 3 : 0)>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
         if (j > 0) {
           // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
           mbar_wait(bar_o_done(t), (g - 1) & 1);

@@ -1,0 +1,414 @@
+// attn_fwd_sm100_2sm.cuh — the D=128 fused attention forward on a CTA PAIR (2 SMs).
+//
+// Same computation as attn_fwd_sm100.cuh (include/tlattn.h; Fig. 18),
+// re-tiled for Blackwell's 2-SM tensor-core mode (tcgen05 .cta_group::2):
+//
+//   cluster of 2 CTAs (leader rank 0, peer rank 1) on one TPC = one unit of 512 query
+//   rows of one (b, h). Query tile t (t = 0, 1) is an M = 256 MMA tile: the leader
+//   holds its rows [r0+256t, +128), the peer [r0+256t+128, +128), each in its own smem
+//   (A operand) and TMEM (accumulators S_t, O_t for its 128 rows).
+//   K_j / V_j blocks are SPLIT between the pair (B operand N-split): the leader holds
+//   keys [0, 64) of K_j and D-columns [0, 64) of V_j, the peer the other halves. Each
+//   SM therefore streams half of every K/V tile from L2 (half the TMA traffic, half the
+//   ring slot size -> a 6-deep ring), and each operand byte read from smem serves 256
+//   query rows instead of 128.
+//   The leader's warps 1/2 issue tcgen05.mma.cta_group::2 (one issuer per query tile);
+//   commits are multicast to both CTAs' barriers. Each CTA runs its own producer and two
+//   softmax warpgroups on its own rows; their S-read / P-written signals arrive on the
+//   leader's barriers (remote mbarrier arrive, cluster scope).
+#pragma once
+#include "attn_fwd_sm100.cuh"
+
+namespace tlattn {
+
+struct KCfg2 {
+  static constexpr int D = 128;
+  static constexpr int Q_TILE_BYTES = BM * D * 2;       // this CTA's 128 rows of tile t
+  static constexpr int K_HALF_CHUNK = 64 * 128;          // 64 keys x 64 elems (SW128 box)
+  static constexpr int SLOT_BYTES = 16384;               // K half (2 x 8 KB) or V half (16 KB)
+  static constexpr int NST = 6;
+  static constexpr int P_TILE_BYTES = BM * BN * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = OFF_Q + TILES * Q_TILE_BYTES;
+  static constexpr int OFF_P = OFF_KV + NST * SLOT_BYTES;
+  static constexpr int OFF_SCHED = OFF_P + TILES * P_TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_SCHED + 32;
+  static constexpr int NUM_BARS = 2 + 2 * NST + 12;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_USED = OFF_TMEMPTR + 16;
+  static constexpr int SMEM_BYTES = SMEM_USED + 1024;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+  static constexpr uint32_t TMEM_O = 2 * BN;
+  static constexpr int UNIT_ROWS = 2 * TILES * BM;  // 512 query rows per CTA pair
+};
+
+// K/V blocks a 256-row tile starting at r0 visits (causal tile skipping on the pair tile)
+__device__ __forceinline__ int tile_nblocks_rows(int r0, int rows, const AttnParams& p) {
+  if (r0 >= p.Sq) return 0;
+  const int n_all = (p.Skv + BN - 1) / BN;
+  if (!p.causal) return n_all;
+  const int r_last = min(r0 + rows - 1, p.Sq - 1);
+  const long long kmax = (long long)r_last + p.Skv - p.Sq;
+  if (kmax < 0) return 0;
+  return min(n_all, (int)(kmax / BN) + 1);
+}
+
+struct Unit2 {
+  int b, h, hkv, r0, n0, n1;
+};
+
+__device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
+  Unit2 U;
+  const int mb_i = u % p.n_mblk;  // n_mblk = ceil(Sq / 512) for this kernel
+  const int bh = u / p.n_mblk;
+  U.h = bh % p.Hq;
+  U.b = bh / p.Hq;
+  const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
+  U.hkv = U.h / (p.Hq / p.Hkv);  // GQA grouping
+  U.r0 = m_blk * KCfg2::UNIT_ROWS;
+  U.n0 = tile_nblocks_rows(U.r0, 2 * BM, p);
+  U.n1 = tile_nblocks_rows(U.r0 + 2 * BM, 2 * BM, p);
+  return U;
+}
+
+template <bool BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
+  using C = KCfg2;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_u32);
+  const uint32_t rank = cluster_ctarank();  // 0 = leader, 1 = peer
+  const bool leader = rank == 0;
+
+  const uint32_t sQ = base + C::OFF_Q;
+  const uint32_t sKV = base + C::OFF_KV;
+  const uint32_t sP = base + C::OFF_P;
+  const uint32_t sSched = base + C::OFF_SCHED;
+  const uint32_t bar0 = base + C::OFF_BAR;
+  const uint32_t bar_q_full = bar0;
+  const uint32_t bar_q_empty = bar0 + 8u;
+  auto bar_kv_full = [&](int s) { return bar0 + 8u * (2 + s); };
+  auto bar_kv_empty = [&](int s) { return bar0 + 8u * (2 + C::NST + s); };
+  auto bar_s_full = [&](int t) { return bar0 + 8u * (2 + 2 * C::NST + t); };
+  auto bar_s_free = [&](int t) { return bar0 + 8u * (4 + 2 * C::NST + t); };
+  auto bar_p_full = [&](int t) { return bar0 + 8u * (6 + 2 * C::NST + t); };
+  auto bar_o_done = [&](int t) { return bar0 + 8u * (8 + 2 * C::NST + t); };
+  auto bar_sched_full = [&](int i) { return bar0 + 8u * (10 + 2 * C::NST + i); };
+  auto bar_sched_empty = [&](int i) { return bar0 + 8u * (12 + 2 * C::NST + i); };
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_q);
+    prefetch_tmap(&p.tm_k);
+    prefetch_tmap(&p.tm_v);
+    mbar_init(bar_q_full, 1);
+    mbar_init(bar_q_empty, 2);
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(bar_kv_full(s), 1);
+      mbar_init(bar_kv_empty(s), 2);
+    }
+    for (int t = 0; t < TILES; ++t) {
+      mbar_init(bar_s_full(t), 1);
+      mbar_init(bar_s_free(t), 8);  // 4 softmax warps in each CTA (leader's copy is used)
+      mbar_init(bar_p_full(t), 8);
+      mbar_init(bar_o_done(t), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_sched_full(i), 1);
+      mbar_init(bar_sched_empty(i), 2 + 8 + 8 + 1);  // issuers, softmax warps x2, peer producer
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<TMEM_COLS>(smem_u32(tmem_ptr_smem));
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / 2-SM TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_smem;
+
+  if (warp < 4) {
+    setmaxnreg_dec<REGS_SMALL>();
+    if (warp == 0) {
+      // =========================== TMA producer (both CTAs) + CLC (leader) =================
+      if (lane == 0) {
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        int unit = blockIdx.x >> 1;
+        int it = 0;
+        const uint32_t lead_q_full = mapa_shared(bar_q_full, 0);
+        for (int k = 0;; ++k) {
+          const int sl = k & 1;
+          mbar_arrive_expect_tx(bar_sched_full(sl), 16);
+          if (leader) {
+            if (k >= 2) mbar_wait(bar_sched_empty(sl), ((k >> 1) - 1) & 1);
+            clc_try_cancel_multicast(sSched + 16 * sl, bar_sched_full(sl));
+          }
+          const Unit2 U = decode_unit2(unit, p);
+          const int nmax = max(U.n0, U.n1);
+          if (k >= 1) mbar_wait(bar_q_empty, (k - 1) & 1);
+          if (leader) {
+            uint32_t qbytes = 0;
+            for (int t = 0; t < TILES; ++t)
+              for (int c = 0; c < 2; ++c)
+                if (U.r0 + 256 * t + 128 * c < p.Sq) qbytes += C::Q_TILE_BYTES;
+            mbar_arrive_expect_tx(bar_q_full, qbytes);
+          }
+#pragma unroll
+          for (int t = 0; t < TILES; ++t) {
+            const int rq = U.r0 + 256 * t + 128 * (int)rank;
+            if (rq < p.Sq) {
+#pragma unroll
+              for (int c = 0; c < D / 64; ++c)
+                tma_load_4d_2sm(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, lead_q_full,
+                                c * 64, U.h, rq, U.b, pol_q);
+            }
+          }
+          // ring order = MMA consumption order: K_0, K_1, V_0, K_2, V_1, ..., V_{nmax-1}
+          for (int q = 0; q < 2 * nmax; ++q, ++it) {
+            const bool is_k = (q == 0) || ((q & 1) && q != 2 * nmax - 1);
+            const int j = (q == 0) ? 0 : (is_k ? (q + 1) >> 1 : (q == 2 * nmax - 1 ? nmax - 1 : (q - 2) >> 1));
+            const int slot = it % C::NST;
+            const int use = it / C::NST;
+            if (use > 0) mbar_wait(bar_kv_empty(slot), (use - 1) & 1);
+            if (leader) mbar_arrive_expect_tx(bar_kv_full(slot), 2 * C::SLOT_BYTES);
+            const uint32_t lead_full = mapa_shared(bar_kv_full(slot), 0);
+            const uint32_t dst = sKV + slot * C::SLOT_BYTES;
+            if (is_k) {  // keys [j*128 + 64*rank, +64), all D (two 64-row x 64-elem boxes)
+#pragma unroll
+              for (int c = 0; c < D / 64; ++c)
+                tma_load_4d_2sm(dst + c * C::K_HALF_CHUNK, &p.tm_k, lead_full, c * 64, U.hkv,
+                                j * BN + 64 * (int)rank, U.b, pol_kv);
+            } else {     // keys [j*128, +128), D-columns [64*rank, +64)
+              tma_load_4d_2sm(dst, &p.tm_v, lead_full, 64 * (int)rank, U.hkv, j * BN, U.b, pol_kv);
+            }
+          }
+          mbar_wait(bar_sched_full(sl), (k >> 1) & 1);
+          const int nxt = clc_query(sSched + 16 * sl);
+          if (!leader) mbar_arrive_cluster(mapa_shared(bar_sched_empty(sl), 0));
+          if (nxt < 0) break;
+          unit = nxt >> 1;
+        }
+      }
+      __syncwarp();
+    } else if ((warp == 1 || warp == 2) && leader) {
+      // =========== MMA issuers (leader only): warp 1 -> tile 0, warp 2 -> tile 1 ===========
+      const int t = warp - 1;
+      if (lane == 0) {
+        constexpr uint32_t FMT = BF16 ? 1u : 0u;
+        // S = Q K^T over the pair: M=256 (rows split), N=128 keys (B split 64/64)
+        const uint32_t IDESC_QK = make_idesc_f16(FMT, 2 * BM, BN, 0, 0, p.neg ? 1u : 0u);
+        // O += P V: M=256, N=D=128 (V's D-columns split 64/64), V MN-major
+        constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, 2 * BM, D, 0, 1, 0);
+        const uint32_t tm_s = tmem_base + t * BN;
+        const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
+        const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
+        const uint32_t pa = sP + t * C::P_TILE_BYTES;
+        int unit = blockIdx.x >> 1;
+        int it = 0;
+        uint32_t cs = 0, cpv = 0;
+        for (int k = 0;; ++k) {
+          const Unit2 U = decode_unit2(unit, p);
+          const int nmax = max(U.n0, U.n1);
+          const int nt = t ? U.n1 : U.n0;
+          const int it0 = it;
+          it += 2 * nmax;
+          auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
+          auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
+          mbar_wait(bar_q_full, k & 1);
+          auto issue_s = [&](int j) {
+            const int sl = kpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
+#ifndef TLATTN_MMA_ONLY
+            if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // both CTAs read S_t
+#endif
+            tc_fence_after();
+            const uint32_t kb = sKV + sl * C::SLOT_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              mma_f16_ss_2sm(tm_s,
+                             make_sdesc_sw128(qa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024),
+                             make_sdesc_sw128(kb + (kk >> 2) * C::K_HALF_CHUNK + (kk & 3) * 32, 16, 1024),
+                             IDESC_QK, kk > 0 ? 1u : 0u);
+            }
+            mma_commit_2sm(bar_s_full(t));
+            mma_commit_2sm(bar_kv_empty(sl));
+            ++cs;
+          };
+          auto issue_pv = [&](int j) {
+            const int sl = vpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
+#ifndef TLATTN_MMA_ONLY
+            mbar_wait(bar_p_full(t), cpv & 1);  // P_t written in both CTAs
+#endif
+            tc_fence_after();
+            const uint32_t vb = sKV + sl * C::SLOT_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              mma_f16_ss_2sm(tm_o,
+                             make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024),
+                             make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024), IDESC_PV,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit_2sm(bar_o_done(t));
+            mma_commit_2sm(bar_kv_empty(sl));
+            ++cpv;
+          };
+          if (nt > 0) {
+            issue_s(0);
+            if (nt == 1) mma_commit_2sm(bar_q_empty);
+            for (int j = 0; j < nt; ++j) {
+              if (j + 1 < nt) {
+                issue_s(j + 1);
+                if (j + 2 == nt) mma_commit_2sm(bar_q_empty);
+              }
+              issue_pv(j);
+            }
+          } else {
+            mma_commit_2sm(bar_q_empty);
+          }
+          for (int j = nt; j < nmax; ++j) {  // blocks only the other tile needs
+            int sl = kpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
+            mma_commit_2sm(bar_kv_empty(sl));
+            sl = vpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
+            mma_commit_2sm(bar_kv_empty(sl));
+          }
+          mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+          const int nxt = clc_query(sSched + 16 * (k & 1));
+          mbar_arrive(bar_sched_empty(k & 1));
+          if (nxt < 0) break;
+          unit = nxt >> 1;
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    setmaxnreg_inc<REGS_SOFTMAX>();
+    // ============== softmax / correction / epilogue (both CTAs, own 128 rows) ==============
+    const int t = (warp - SOFTMAX_WARP0) >> 2;
+    const int q4 = warp & 3;
+    const int lr = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t tm_s = tmem_base + lane_off + t * BN;
+    const uint32_t tm_o = tmem_base + lane_off + C::TMEM_O + t * D;
+    const uint32_t p_row = sP + t * C::P_TILE_BYTES + lr * 128;
+    const uint32_t lead_s_free = mapa_shared(bar_s_free(t), 0);
+    const uint32_t lead_p_full = mapa_shared(bar_p_full(t), 0);
+    const float c = p.c_log2;
+    int unit = blockIdx.x >> 1;
+    uint32_t g = 0;
+    for (int k = 0;; ++k) {
+      const Unit2 U = decode_unit2(unit, p);
+#ifdef TLATTN_MMA_ONLY
+      const int nt = 0;
+#else
+      const int nt = t ? U.n1 : U.n0;
+#endif
+      const int row = U.r0 + 256 * t + 128 * (int)rank + lr;
+      const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
+      float m = -INFINITY;
+      float l = 0.f;
+      for (int j = 0; j < nt; ++j, ++g) {
+        mbar_wait(bar_s_full(t), g & 1);
+        tc_fence_after();
+        uint32_t sr[BN];
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc)
+          tmem_ld32(tm_s + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + cc * 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(lead_s_free);
+        float m_new, alpha, sum;
+        uint32_t pk[BN / 2];
+        softmax_row_block<BF16, 0>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
+        if (j > 0) {
+          mbar_wait(bar_o_done(t), (g - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+            for (int cc = 0; cc < D / 32; ++cc) {
+              uint32_t ov[32];
+              tmem_ld32(tm_o + cc * 32, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              tmem_st32(tm_o + cc * 32, ov);
+            }
+            tmem_st_wait();
+          }
+        }
+#pragma unroll
+        for (int ch = 0; ch < BN / 64; ++ch) {
+#pragma unroll
+          for (int uu = 0; uu < 8; ++uu) {
+            const uint32_t addr = p_row + ch * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
+            const int w = ch * 32 + uu * 4;
+            st_shared_v4(addr, pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(lead_p_full);
+        l = l * alpha + sum;
+        m = m_new;
+      }
+      if (nt > 0) {
+        mbar_wait(bar_o_done(t), (g - 1) & 1);
+        tc_fence_after();
+      }
+      const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
+      const bool row_ok = row < p.Sq;
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
+                      ((((size_t)U.b * p.Sq + (row_ok ? row : 0)) * p.Hq + U.h) * D) * 2;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t ov[32];
+        if (nt > 0) {
+          tmem_ld32(tm_o + cc * 32, ov);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = 0u;
+        }
+        uint32_t pkd[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
+        if (row_ok) {
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4)
+            st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2],
+                         pkd[4 * v4 + 3]);
+        }
+      }
+      if (p.lse != nullptr && row_ok) {
+        p.lse[((size_t)U.b * p.Hq + U.h) * p.Sq + row] =
+            (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+      }
+      tc_fence_before();
+      mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+      const int nxt = clc_query(sSched + 16 * (k & 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_sched_empty(k & 1), 0));
+      if (nxt < 0) break;
+      unit = nxt >> 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();  // both CTAs finished with TMEM / smem of the pair
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace tlattn

@@ -11,11 +11,13 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "../../include/tlattn.h"
 #include "attn_fwd_sm100.cuh"
+#include "attn_fwd_sm100_2sm.cuh"
 
 using namespace tlattn;
 
@@ -27,7 +29,7 @@ struct DeviceInfo {
   int sm_count = 0;
   int major = 0, minor = 0;
   bool ok = false;
-  bool smem_set[4] = {false, false, false, false};
+  bool smem_set[6] = {false, false, false, false, false, false};
 };
 
 constexpr int kMaxDevices = 64;
@@ -93,17 +95,44 @@ int validate(const void* q, const void* k, const void* v, const void* o, const f
 }
 
 bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
-                 int Bn, int S, int H, int D) {
+                 int Bn, int S, int H, int D, unsigned box_rows = 128) {
   const cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)Bn};
   const cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2,
                                  (cuuint64_t)S * H * D * 2};
-  const cuuint32_t box[4] = {64, 1, 128, 1};
+  const cuuint32_t box[4] = {64, 1, box_rows, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+template <bool BF16>
+int launch_2sm(const AttnParams& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
+  auto kern = tl_attn_fwd_kernel_2sm<BF16>;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di.smem_set[inst]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               KCfg2::SMEM_BYTES) != cudaSuccess) {
+        cudaGetLastError();
+        return TL_ERR_CUDA;
+      }
+      di.smem_set[inst] = true;
+    }
+  }
+  kern<<<2 * prm.n_units, NUM_THREADS, KCfg2::SMEM_BYTES, stream>>>(prm);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  return TL_OK;
+}
+
+// Kernel selection: D=128 runs on CTA pairs (2-SM tcgen05), D=64 on single CTAs.
+// TLATTN_KERNEL=1cta forces the single-CTA kernel for D=128 (A/B comparisons only).
+bool use_2sm(int D) {
+  if (D != 128) return false;
+  const char* e = std::getenv("TLATTN_KERNEL");
+  return !(e && std::strcmp(e, "1cta") == 0);
 }
 
 template <int D, bool BF16>
@@ -139,10 +168,11 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   auto enc = get_encode();
   if (!enc) return TL_ERR_CUDA;
 
+  const bool pair = use_2sm(D);
   AttnParams prm;
   std::memset(&prm, 0, sizeof(prm));
   if (!encode_bshd(enc, &prm.tm_q, q, dtype, B, Sq, Hq, D) ||
-      !encode_bshd(enc, &prm.tm_k, k, dtype, B, Skv, Hkv, D) ||
+      !encode_bshd(enc, &prm.tm_k, k, dtype, B, Skv, Hkv, D, pair ? 64u : 128u) ||
       !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D))
     return TL_ERR_CUDA;
   prm.o = o;
@@ -154,7 +184,8 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   prm.Skv = Skv;
   prm.causal = causal;
   prm.c_log2 = std::fabs(scale) * 1.4426950408889634f;
-  prm.n_mblk = (Sq + TILES * BM - 1) / (TILES * BM);
+  const int unit_rows = pair ? KCfg2::UNIT_ROWS : TILES * BM;
+  prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
   prm.n_units = B * Hq * prm.n_mblk;
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
@@ -162,7 +193,8 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool bf = dtype == TL_DTYPE_BF16;
-  if (D == 128) rc = bf ? launch<128, true>(prm, *di, 0, st) : launch<128, false>(prm, *di, 1, st);
+  if (pair) rc = bf ? launch_2sm<true>(prm, *di, 4, st) : launch_2sm<false>(prm, *di, 5, st);
+  else if (D == 128) rc = bf ? launch<128, true>(prm, *di, 0, st) : launch<128, false>(prm, *di, 1, st);
   else rc = bf ? launch<64, true>(prm, *di, 2, st) : launch<64, false>(prm, *di, 3, st);
   if (rc == TL_OK) g_last_launches = 1;
   return rc;
