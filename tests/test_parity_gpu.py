@@ -159,3 +159,36 @@ def test_bad_args_raise_before_launch():
         tl_attn_fwd(q, k, v, o, None, 1, 2, 2, 128, 128, 96, 0, 0.1, 1)
     assert e.value.status == 2
     _ = oracle, odt, to_bits  # imported for parity with the other GPU test modules
+
+
+@pytest.mark.parametrize("mode", ["head", "batch"])
+def test_shards_equal_unsharded_slices_bitwise(mode):
+    """Multi-GPU partition (run here as successive shards on one GPU): every rank's
+    tl_attn_fwd over its shard, generated from global indices, equals the matching slice
+    of the unsharded output bitwise (deterministic kernel, no cross-unit reduction)."""
+    from paper_2504_17577_b200.dist import make_shard
+    from paper_2504_17577_b200.inputs import gen_qkv
+    Bz, Hq, Hkv, S, D = 4, 8, 4, 640, 128
+    q, k, v = gen_qkv(Bz, Hq, Hkv, S, S, D, BF, 77, "cuda")
+    o_full, l_full = attention(q, k, v, causal=True)
+    for r in range(4):
+        sh = make_shard(mode, r, 4, Bz, Hq, Hkv)
+        ql, kl, vl = gen_qkv(Bz, Hq, Hkv, S, S, D, BF, 77, "cuda", b_slice=sh.b, hq_slice=sh.hq,
+                             hkv_slice=sh.hkv)
+        o, l = attention(ql, kl, vl, causal=True)
+        torch.cuda.synchronize()
+        assert torch.equal(o, o_full[sh.b, :, sh.hq]) and torch.equal(l, l_full[sh.b, sh.hq])
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_single_cta_kernel_at_d128(causal, monkeypatch):
+    """D=128 normally runs on CTA pairs; the single-CTA kernel (TLATTN_KERNEL=1cta) stays
+    correct too, and both kernels agree within rounding."""
+    q, k, v = gen(2, 4, 2, 700, 700, 128, BF, 91)
+    o2, l2 = attention(q, k, v, causal=causal)
+    monkeypatch.setenv("TLATTN_KERNEL", "1cta")
+    check_against_oracle(q, k, v, causal, default_scale(128), label="1cta")
+    o1, l1 = attention(q, k, v, causal=causal)
+    torch.cuda.synchronize()
+    assert (o1.float() - o2.float()).abs().max().item() < 2e-2
+    assert (l1 - l2).abs().max().item() < 1e-4
