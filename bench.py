@@ -18,7 +18,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import sys
 import threading
@@ -280,7 +279,9 @@ def run_ours(args, world, rank, local):
     achieved = flop_local / (kern_ms * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["burst"], "unit": UNIT,
                 "frac": achieved / pk["burst"], "traffic": ncu_traffic(cfg.name, world),
-                "peak_source": pk["source"] + " bf16 burst", "kernel": "tl_attn_fwd_kernel<128,bf16>",
+                "peak_source": pk["source"] + " bf16 burst",
+                "kernel": ("tl_attn_fwd_kernel_2sm<bf16> (CTA pair)" if cfg.D == 128
+                           else f"tl_attn_fwd_kernel<{cfg.D},{cfg.dtype_name}>"),
                 "frac_of_sustained": achieved / pk["sustained"],
                 "frac_of_spec_2250": achieved / 2250.0}
 
