@@ -148,6 +148,11 @@ struct Exp2Poly {
 #ifndef TLATTN_EXP_VARIANT
 #define TLATTN_EXP_VARIANT 0
 #endif
+#ifdef TLATTN_EMU_OVERRIDE  // experiments only
+#define TLATTN_EMU_2SM TLATTN_EMU_OVERRIDE
+#else
+#define TLATTN_EMU_2SM 0
+#endif
 template <int EMU>
 __host__ __device__ constexpr bool emu_pair(int q) {
   return TLATTN_EXP_VARIANT == 2 ? true
@@ -158,6 +163,40 @@ __host__ __device__ constexpr bool emu_pair(int q) {
        : false;
 }
 
+
+// p = exp2(s*c - m) for one 128-column row with paired FFMA2, FADD2 row sums (two
+// accumulators), P packed RN to the dtype; emu_pair<EMU>() column pairs use Exp2Poly.
+template <bool BF16, int EMU>
+__device__ __forceinline__ void exp_row(const float* s, float c, float m_use,
+                                        uint32_t (&pk)[BN / 2], float& sum0, float& sum1) {
+  const uint64_t c2 = f2pack(c, c);
+  const uint64_t nm2 = f2pack(-m_use, -m_use);
+  const Exp2Poly poly;
+  uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+  for (int q = 0; q < BN / 2; ++q) {
+    const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
+    float p0, p1;
+    if (TLATTN_EXP_VARIANT == 3) {
+      f2unpack(x2, p0, p1);
+    } else if (emu_pair<EMU>(q)) {
+      poly(x2, p0, p1);
+    } else {
+      float x0, x1;
+      f2unpack(x2, x0, x1);
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
+    else acc0 = fadd2(acc0, f2pack(p0, p1));
+    pk[q] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+  }
+  float a0, a1, b0, b1;
+  f2unpack(acc0, a0, a1);
+  f2unpack(acc1, b0, b1);
+  sum0 = a0 + b0;
+  sum1 = a1 + b1;
+}
 
 // One K/V block of the online softmax for the row this thread owns (Fig. 18
 // P:L660-679): mask (diagonal / tail blocks only), row max, conditional running-max
@@ -191,50 +230,13 @@ __device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, in
   const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
   alpha_out = ex2(m - m_use);                              // scores_scale
   m_new_out = m_new;
-  // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8)
-  float sum0 = 0.f, sum1 = 0.f;
-  if (masked) {
-#pragma unroll
-    for (int cc = 0; cc < BN; cc += 2) {
-      float p0 = ex2(fmaf(s[cc], c, -m_use));
-      float p1 = ex2(fmaf(s[cc + 1], c, -m_use));
-      if (s[cc] == -INFINITY) p0 = 0.f;
-      if (s[cc + 1] == -INFINITY) p1 = 0.f;
-      sum0 += p0;
-      sum1 += p1;
-      pk[cc / 2] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
-    }
-  } else {
-    // unmasked block: paired FFMA2 for s*c - m, FADD2 row sums; emu_pair() column pairs
-    // take exp2 on the FMA pipe (Exp2Poly), the rest on MUFU
-    const uint64_t c2 = f2pack(c, c);
-    const uint64_t nm2 = f2pack(-m_use, -m_use);
-    const Exp2Poly poly;
-    uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
-#pragma unroll
-    for (int q = 0; q < BN / 2; ++q) {
-      const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
-      float p0, p1;
-      if (TLATTN_EXP_VARIANT == 3) {
-        f2unpack(x2, p0, p1);
-      } else if (emu_pair<EMU>(q)) {
-        poly(x2, p0, p1);
-      } else {
-        float x0, x1;
-        f2unpack(x2, x0, x1);
-        p0 = ex2(x0);
-        p1 = ex2(x1);
-      }
-      if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
-      else acc0 = fadd2(acc0, f2pack(p0, p1));
-      pk[q] = pack2<BF16>(p0, p1);
-    }
-    float a0, a1, b0, b1;
-    f2unpack(acc0, a0, a1);
-    f2unpack(acc1, b0, b1);
-    sum0 = a0 + b0;
-    sum1 = a1 + b1;
-  }
+  // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8).
+  // c > 0 always (scale = 0 arrives as a tiny positive c, host side), so a masked
+  // s = -inf gives exp2(-inf) = 0 exactly and masked blocks use the same paired loop
+  // (MUFU only); unmasked blocks offload emu_pair<EMU>() columns to the FMA pipe.
+  float sum0, sum1;
+  if (masked) exp_row<BF16, 0>(s, c, m_use, pk, sum0, sum1);  // diagonal / tail: MUFU only
+  else exp_row<BF16, EMU>(s, c, m_use, pk, sum0, sum1);
   sum_out = sum0 + sum1;
 }
 

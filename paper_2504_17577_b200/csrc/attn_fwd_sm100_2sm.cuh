@@ -327,7 +327,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         if (lane == 0) mbar_arrive_cluster(lead_s_free);
         float m_new, alpha, sum;
         uint32_t pk[BN / 2];
-        softmax_row_block<BF16, 0>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
+        softmax_row_block<BF16, TLATTN_EMU_2SM>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
         if (j > 0) {
           mbar_wait(bar_o_done(t), (g - 1) & 1);
           tc_fence_after();

@@ -184,6 +184,10 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   prm.Skv = Skv;
   prm.causal = causal;
   prm.c_log2 = std::fabs(scale) * 1.4426950408889634f;
+  // scale = 0 (uniform attention): use a tiny positive c instead, so masked scores
+  // (-inf) still map to exp2(-inf) = 0 in the kernel's single exp path; with |s| << 1e28
+  // every allowed p is exactly 1 and LSE = ln|J| up to ~1e-28.
+  if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;
   const int unit_rows = pair ? KCfg2::UNIT_ROWS : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
   prm.n_units = B * Hq * prm.n_mblk;

@@ -35,9 +35,11 @@ def main():
         evs.append((s, e))
     torch.cuda.synchronize()
     if a.time:
-        for s, e in evs:
-            ms = s.elapsed_time(e)
-            print(f"{cfg.name}: {ms:.3f} ms  {cfg.flops() / ms / 1e9:.1f} TFLOP/s")
+        import statistics
+        ms_all = [s.elapsed_time(e) for s, e in evs[1:]] or [evs[0][0].elapsed_time(evs[0][1])]
+        ms = statistics.median(ms_all)
+        print(f"{cfg.name}: median {ms:.3f} ms  {cfg.flops() / ms / 1e9:.1f} TFLOP/s "
+              f"(min {min(ms_all):.3f} max {max(ms_all):.3f}, n={len(ms_all)})")
 
 
 if __name__ == "__main__":
