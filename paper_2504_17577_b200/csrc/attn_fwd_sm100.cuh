@@ -49,7 +49,29 @@ struct AttnParams {
   int neg;           // scale < 0: negate A (= Q) in the QK^T instruction descriptor
   int n_mblk;        // ceil(Sq / 256)
   int n_units;       // B * Hq * n_mblk
+  unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
 };
+
+// Debug-only pipeline trace (compile with -DTLATTN_TRACE): clock64 stamps of the first
+// unit of CTA 0 (the pair leader), used to inspect the MMA / softmax overlap.
+#ifdef TLATTN_TRACE
+#define TL_TRACE(k, idx)                                                          \
+  do {                                                                            \
+    if (p.trace != nullptr && blockIdx.x == 0 && (k) == 0) p.trace[(idx)] = clock64(); \
+  } while (0)
+#define TL_TRACE2(k, idx)                                                                \
+  do {                                                                                   \
+    if (p.trace != nullptr && blockIdx.x < 2 && (k) < 4)                                 \
+      p.trace[(idx) + 200 * (k) + 8000 * blockIdx.x] = clock64();                        \
+  } while (0)
+#else
+#define TL_TRACE2(k, idx) \
+  do {                    \
+  } while (0)
+#define TL_TRACE(k, idx) \
+  do {                   \
+  } while (0)
+#endif
 
 template <int D>
 struct KCfg {
@@ -167,33 +189,47 @@ __host__ __device__ constexpr bool emu_pair(int q) {
 // p = exp2(s*c - m) for one 128-column row with paired FFMA2, FADD2 row sums (two
 // accumulators), P packed RN to the dtype; emu_pair<EMU>() column pairs use Exp2Poly.
 template <bool BF16, int EMU>
-__device__ __forceinline__ void exp_row(const float* s, float c, float m_use,
-                                        uint32_t (&pk)[BN / 2], float& sum0, float& sum1) {
+__device__ __forceinline__ void exp_row(float* s, float c, float m_use, uint32_t (&pk)[BN / 2],
+                                        float& sum0, float& sum1) {
   const uint64_t c2 = f2pack(c, c);
   const uint64_t nm2 = f2pack(-m_use, -m_use);
-  const Exp2Poly poly;
-  uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
+  // Phases, 32 columns at a time (independent work back to back so one warp keeps MUFU
+  // fed): x = s*c - m (FFMA2), then p = exp2(x) (MUFU or Exp2Poly), then row sums (FADD2,
+  // 4 accumulators) and RN packing.
+  uint64_t acc[4];
 #pragma unroll
-  for (int q = 0; q < BN / 2; ++q) {
-    const uint64_t x2 = ffma2(f2pack(s[2 * q], s[2 * q + 1]), c2, nm2);
-    float p0, p1;
-    if (TLATTN_EXP_VARIANT == 3) {
-      f2unpack(x2, p0, p1);
-    } else if (emu_pair<EMU>(q)) {
-      poly(x2, p0, p1);
-    } else {
-      float x0, x1;
-      f2unpack(x2, x0, x1);
-      p0 = ex2(x0);
-      p1 = ex2(x1);
+  for (int a = 0; a < 4; ++a) acc[a] = f2pack(0.f, 0.f);
+#pragma unroll
+  for (int h = 0; h < BN; h += 32) {
+    float x[32];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint64_t x2 = ffma2(f2pack(s[h + 2 * q], s[h + 2 * q + 1]), c2, nm2);
+      f2unpack(x2, x[2 * q], x[2 * q + 1]);
     }
-    if (q & 1) acc1 = fadd2(acc1, f2pack(p0, p1));
-    else acc0 = fadd2(acc0, f2pack(p0, p1));
-    pk[q] = pack2<BF16>(p0, p1);  // P rounded RN to dtype (R8)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int qq = h / 2 + q;
+      if (TLATTN_EXP_VARIANT == 3) {
+      } else if (emu_pair<EMU>(qq)) {
+        const Exp2Poly poly;
+        poly(f2pack(x[2 * q], x[2 * q + 1]), x[2 * q], x[2 * q + 1]);
+      } else {
+        x[2 * q] = ex2(x[2 * q]);
+        x[2 * q + 1] = ex2(x[2 * q + 1]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      acc[q & 3] = fadd2(acc[q & 3], f2pack(x[2 * q], x[2 * q + 1]));
+      pk[h / 2 + q] = pack2<BF16>(x[2 * q], x[2 * q + 1]);  // P rounded RN (R8)
+    }
   }
+  const uint64_t t0 = fadd2(acc[0], acc[1]);
+  const uint64_t t1 = fadd2(acc[2], acc[3]);
   float a0, a1, b0, b1;
-  f2unpack(acc0, a0, a1);
-  f2unpack(acc1, b0, b1);
+  f2unpack(t0, a0, a1);
+  f2unpack(t1, b0, b1);
   sum0 = a0 + b0;
   sum1 = a1 + b1;
 }

@@ -316,6 +316,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
       float l = 0.f;
       for (int j = 0; j < nt; ++j, ++g) {
         mbar_wait(bar_s_full(t), g & 1);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 0);
         tc_fence_after();
         uint32_t sr[BN];
 #pragma unroll
@@ -325,11 +326,14 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(lead_s_free);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 1);
         float m_new, alpha, sum;
         uint32_t pk[BN / 2];
         softmax_row_block<BF16, TLATTN_EMU_2SM>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 2);
         if (j > 0) {
           mbar_wait(bar_o_done(t), (g - 1) & 1);
+          if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 3);
           tc_fence_after();
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
@@ -357,6 +361,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(lead_p_full);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 4);
         l = l * alpha + sum;
         m = m_new;
       }

@@ -353,6 +353,14 @@ __device__ __forceinline__ void clc_try_cancel_multicast(uint32_t resp_smem, uin
       : "memory");
 }
 
+// ------------------------------------------------------------------ named barriers
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ------------------------------------------------------------------ register rebalancing
 // Per-warpgroup register budget (all 4 warps of the warpgroup must execute it).
 template <uint32_t N>

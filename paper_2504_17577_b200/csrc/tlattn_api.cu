@@ -24,6 +24,7 @@ using namespace tlattn;
 namespace {
 
 thread_local int g_last_launches = 0;
+unsigned long long* g_trace = nullptr;  // debug builds only (tl_attn_debug_trace)
 
 struct DeviceInfo {
   int sm_count = 0;
@@ -194,6 +195,7 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
   prm.neg = scale < 0.f ? 1 : 0;
+  prm.trace = g_trace;
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool bf = dtype == TL_DTYPE_BF16;
@@ -327,5 +329,17 @@ extern "C" const char* tl_attn_strerror(int status) {
 }
 
 extern "C" int tl_attn_version(void) { return TLATTN_VERSION; }
+
+// Debug hook (not part of include/tlattn.h): device buffer of >= 8000 u64 that receives
+// clock64 pipeline events of CTA 0 in builds compiled with -DTLATTN_TRACE.
+extern "C" int tl_attn_debug_trace(void* dev_buf) {
+#ifdef TLATTN_TRACE
+  g_trace = static_cast<unsigned long long*>(dev_buf);
+  return TL_OK;
+#else
+  (void)dev_buf;
+  return TL_ERR_UNSUPPORTED;
+#endif
+}
 
 extern "C" int tl_attn_last_launch_count(void) { return g_last_launches; }
