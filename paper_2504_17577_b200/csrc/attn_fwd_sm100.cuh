@@ -41,6 +41,7 @@ struct AttnParams {
   CUtensorMap tm_q;  // BSHD as 4-D (D, Hq, Sq, B), box (64, 1, 128, 1), SWIZZLE_128B
   CUtensorMap tm_k;  // (D, Hkv, Skv, B)
   CUtensorMap tm_v;
+  CUtensorMap tm_o;  // output, same geometry as tm_q (TMA-store epilogue)
   void* o;           // BSHD output
   float* lse;        // [B][Hq][Sq] or nullptr
   int B, Hq, Hkv, Sq, Skv;

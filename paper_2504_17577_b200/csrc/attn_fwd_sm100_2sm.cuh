@@ -348,6 +348,12 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
             tmem_st_wait();
           }
         }
+        if (j == 0 && g > 0) {
+          // P_t smem held the previous unit's O tile for its TMA store: wait until the
+          // bulk store has read it (one issuing thread), then release the warpgroup
+          if (lr == 0) tma_store_wait_read<0>();
+          named_bar_sync(1 + t, 128);
+        }
 #pragma unroll
         for (int ch = 0; ch < BN / 64; ++ch) {
 #pragma unroll
@@ -371,8 +377,13 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
       }
       const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
       const bool row_ok = row < p.Sq;
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
-                      ((((size_t)U.b * p.Sq + (row_ok ? row : 0)) * p.Hq + U.h) * D) * 2;
+      if (nt == 0) {  // no PV this unit: P_t may still feed the previous unit's O store
+        if (lr == 0) tma_store_wait_read<0>();
+        named_bar_sync(1 + t, 128);
+      }
+      // O tile -> P_t smem (free: the unit's last PV is done) in the TMA SWIZZLE_128B box
+      // layout, then one thread stores it with two bulk-tensor stores (coalesced; rows
+      // beyond Sq are clipped by the tensor map)
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t ov[32];
@@ -387,12 +398,23 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
-        if (row_ok) {
 #pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4)
-            st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2],
-                         pkd[4 * v4 + 3]);
+        for (int v4 = 0; v4 < 4; ++v4) {
+          const int uu = (cc & 1) * 4 + v4;  // 16-B unit within the 128-B row of chunk cc/2
+          const uint32_t addr = p_row + (cc >> 1) * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
+          st_shared_v4(addr, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2], pkd[4 * v4 + 3]);
         }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, 128);
+      if (lr == 0) {
+        const int row0 = U.r0 + 256 * t + 128 * (int)rank;
+        if (row0 < p.Sq) {
+#pragma unroll
+          for (int c2 = 0; c2 < D / 64; ++c2)
+            tma_store_4d(&p.tm_o, sP + t * C::P_TILE_BYTES + c2 * CHUNK_BYTES, c2 * 64, U.h, row0, U.b);
+        }
+        tma_store_commit();
       }
       if (p.lse != nullptr && row_ok) {
         p.lse[((size_t)U.b * p.Hq + U.h) * p.Sq + row] =
@@ -408,6 +430,8 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
     }
   }
 
+  if (warp >= SOFTMAX_WARP0 && ((warp - SOFTMAX_WARP0) & 3) == 0 && lane == 0)
+    tma_store_wait_all<0>();  // O stores complete before the CTA's smem goes away
   tc_fence_before();
   cluster_sync();  // both CTAs finished with TMEM / smem of the pair
   if (warp == 1) {

@@ -174,7 +174,8 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   std::memset(&prm, 0, sizeof(prm));
   if (!encode_bshd(enc, &prm.tm_q, q, dtype, B, Sq, Hq, D) ||
       !encode_bshd(enc, &prm.tm_k, k, dtype, B, Skv, Hkv, D, pair ? 64u : 128u) ||
-      !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D))
+      !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D) ||
+      !encode_bshd(enc, &prm.tm_o, o, dtype, B, Sq, Hq, D))
     return TL_ERR_CUDA;
   prm.o = o;
   prm.lse = lse;
