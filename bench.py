@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-period-ms", type=float, default=5.0,
+                    help="NVML clock sampling period during the timed region (0 = off)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to exercise N>1 on one GPU)")
     return ap.parse_args()
@@ -77,6 +79,9 @@ class ClockSampler:
         self.samples, self.reasons, self.period = [], 0, period
         self.max_mhz = None
         self._stop = threading.Event()
+        self.nv = None
+        if period <= 0:
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -278,7 +283,7 @@ def run_ours(args, world, rank, local):
         attention(q, k, v, causal=cfg.causal, scale=cfg.scale, out=o, lse_out=lse)
         launches[0] += tl_attn_last_launch_count()  # kernels this call launched (1)
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_period_ms / 1000.0) as clk:
         total_ms, kern_ms = time_device(step, args.steps, args.warmup, world)
     timed_launches = launches[0] - args.warmup * tl_attn_last_launch_count()
     flop = cfg.flops()
