@@ -15,6 +15,9 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#ifdef TLATTN_DBG
+#include <cstdio>
+#endif
 
 namespace tlattn {
 
@@ -85,7 +88,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   const uint64_t t0 = globaltimer();
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS) __trap();
+    if ((++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS) {
+#ifdef TLATTN_DBG
+      printf("watchdog: block %d thread %d barrier smem 0x%x parity %u\n", blockIdx.x, threadIdx.x,
+             bar, parity);
+      return;
+#else
+      __trap();
+#endif
+    }
   }
 }
 
