@@ -192,3 +192,51 @@ def test_single_cta_kernel_at_d128(causal, monkeypatch):
     torch.cuda.synchronize()
     assert (o1.float() - o2.float()).abs().max().item() < 2e-2
     assert (l1 - l2).abs().max().item() < 1e-4
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,S,D,dtype,causal", [
+    (2, 4, 2, 520, 128, F16, True),    # fp16 on the CTA-pair kernel
+    (2, 4, 4, 520, 64, BF, True),      # bf16 on the single-CTA D=64 kernel
+    (1, 8, 1, 777, 128, BF, False),    # MQA, ragged
+])
+def test_parity_dtype_kernel_matrix(B, Hq, Hkv, S, D, dtype, causal):
+    q, k, v = gen(B, Hq, Hkv, S, S, D, dtype, 101 + S)
+    check_against_oracle(q, k, v, causal, default_scale(D), label=f"{dtype} D{D}")
+
+
+def test_cuda_graph_capture_replays_identically():
+    """tl_attn_fwd allocates nothing and never syncs, so it is graph-capturable; replays
+    reproduce the eager result bitwise."""
+    q, k, v = gen(2, 4, 2, 512, 512, 128, BF, 111)
+    o_ref, l_ref = attention(q, k, v, causal=True)
+    o = torch.empty_like(q)
+    lse = torch.empty_like(l_ref)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        attention(q, k, v, causal=True, out=o, lse_out=lse)  # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        attention(q, k, v, causal=True, out=o, lse_out=lse)
+    o.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_ref) and torch.equal(lse, l_ref)
+
+
+def test_concurrent_streams():
+    """Two independent problems on two streams at once give the same results as serially."""
+    a = gen(1, 4, 4, 640, 640, 128, BF, 121)
+    b = gen(2, 2, 2, 384, 384, 64, F16, 122)
+    ra = attention(*a, causal=True)
+    rb = attention(*b, causal=False)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        oa = attention(*a, causal=True)
+    with torch.cuda.stream(s2):
+        ob = attention(*b, causal=False)
+    torch.cuda.synchronize()
+    assert torch.equal(oa[0], ra[0]) and torch.equal(ob[0], rb[0])
