@@ -564,6 +564,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
 
       for (int j = 0; j < nt; ++j, ++g) {
         mbar_wait(bar_s_full(t), g & 1);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 0);
         tc_fence_after();
         uint32_t sr[BN];
 #pragma unroll
@@ -573,13 +574,16 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s_free(t));  // S_t may be overwritten by QK^T(j+1)
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 1);
 
         float m_new, alpha, sum;
         uint32_t pk[BN / 2];
         softmax_row_block<BF16, (D == 64 ? 3 : 0)>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 2);
         if (j > 0) {
           // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
           mbar_wait(bar_o_done(t), (g - 1) & 1);
+          if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 3);
           tc_fence_after();
           if (__any_sync(0xffffffffu, alpha != 1.f)) {  // acc_o *= scores_scale
 #pragma unroll
@@ -611,6 +615,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_full(t));
+        if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 4);
         l = l * alpha + sum;  // logsum = logsum * scores_scale + scores_sum
         m = m_new;
       }
