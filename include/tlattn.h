@@ -99,6 +99,25 @@ int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_h, void* o_
 uint64_t tl_attn_host_workspace_bytes(int B, int Hq, int Hkv, int Sq, int Skv, int D,
                                       int with_lse);
 
+/*
+ * tl_gemm — dense GEMM C = A · B (Fig. 1 / Fig. 16 "Matmul",
+ * P:L58-157; benchmark shapes Table 2), on the current device.
+ *
+ *   a      device pointer, A [M][K] row-major (K contiguous), fp16 or bf16
+ *   b      device pointer, B [K][N] row-major (N contiguous), same dtype
+ *   c      device pointer, C [M][N] row-major, same dtype, written in full
+ *   M,N,K  sizes >= 1; N and K multiples of 8 (16-byte TMA row strides)
+ *   dtype  TL_DTYPE_F16 or TL_DTYPE_BF16; accumulation is fp32, C is rounded RN
+ *   stream cudaStream_t as void*
+ *
+ * Ownership / synchronisation as tl_attn_fwd (caller-owned buffers, stream-ordered, no
+ * allocation, graph-capturable). c must not alias a or b.
+ * Errors: TL_ERR_INVALID_VALUE (NULL pointer, size < 1, bad dtype), TL_ERR_UNSUPPORTED
+ * (N or K not a multiple of 8, pointer not 16-byte aligned, too many tiles, device not
+ * sm_100), TL_ERR_CUDA. Argument errors are returned before any CUDA call.
+ */
+int tl_gemm(const void* a, const void* b, void* c, int M, int N, int K, int dtype, void* stream);
+
 /* Static, NUL-terminated description of a tl_status code. Never NULL. */
 const char* tl_attn_strerror(int status);
 

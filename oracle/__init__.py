@@ -13,6 +13,8 @@ from .oracle import (  # noqa: F401
     attn_rows_parallel,
     attn_full,
     brute_force,
+    gemm_rows,
+    gemm_rows_parallel,
     ORACLE_F16,
     ORACLE_BF16,
 )

@@ -55,6 +55,11 @@ int oracle_brute_force(const uint16_t* q, const uint16_t* k, const uint16_t* v, 
                        int causal, double scale, long b, long h,
                        double* s_out, double* p_out, double* o_out, double* lse_out);
 
+/* Plain GEMM (Fig. 16 Matmul): rows[nrows] of C = A[M][K] B[K][N] in fp64,
+ * c_out is nrows x N. */
+int oracle_gemm_rows(const uint16_t* a, const uint16_t* b, int dtype, long M, long N, long K,
+                     const long* rows, long nrows, double* c_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ ORACLE_BF16 = 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRC = [os.path.join(_HERE, "attn_oracle.c")]
+_SRC = [os.path.join(_HERE, "attn_oracle.c"), os.path.join(_HERE, "gemm_oracle.c")]
 _lock = threading.Lock()
 _lib = None
 
@@ -54,6 +54,8 @@ def _load():
             lib.oracle_brute_force.argtypes = [P16, P16, P16, I, L, L, L, L, L, L, I, D, L, L,
                                                PD, PD, PD, PD]
             lib.oracle_brute_force.restype = I
+            lib.oracle_gemm_rows.argtypes = [P16, P16, I, L, L, L, PL, L, PD]
+            lib.oracle_gemm_rows.restype = I
             _lib = lib
     return _lib
 
@@ -139,3 +141,33 @@ def brute_force(q, k, v, dtype, causal, scale, b, h):
     if rc != 0:
         raise ValueError(f"oracle_brute_force rejected its arguments (rc={rc})")
     return S, P, O, lse
+
+
+def gemm_rows(a, b, dtype, rows):
+    """Rows of C = A @ B (A [M,K], B [K,N] uint16 bit patterns) in float64."""
+    lib = _load()
+    assert a.ndim == 2 and b.ndim == 2 and a.shape[1] == b.shape[0]
+    M, K = a.shape
+    N = b.shape[1]
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    c = np.zeros((rows.shape[0], N), np.float64)
+    rc = lib.oracle_gemm_rows(_p16(a), _p16(b), dtype, M, N, K,
+                              rows.ctypes.data_as(ctypes.POINTER(ctypes.c_long)), rows.shape[0],
+                              _pd(c))
+    if rc != 0:
+        raise ValueError(f"oracle_gemm_rows rejected its arguments (rc={rc})")
+    return c
+
+
+def gemm_rows_parallel(a, b, dtype, rows, threads=None):
+    threads = threads or len(os.sched_getaffinity(0))
+    rows = list(rows)
+    chunks = [rows[i::threads] for i in range(threads) if rows[i::threads]]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(lambda r: gemm_rows(a, b, dtype, r), chunks))
+    out = np.zeros((len(rows), b.shape[1]), np.float64)
+    pos = {r: i for i, r in enumerate(rows)}
+    for ch, c in zip(chunks, res):
+        for k, r in enumerate(ch):
+            out[pos[r]] = c[k]
+    return out

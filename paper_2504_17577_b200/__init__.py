@@ -15,6 +15,8 @@ from .tlattn import (  # noqa: F401
     TlAttnError,
     attention,
     dtype_code,
+    gemm,
+    tl_gemm,
     load_library,
     tl_attn_fwd,
     tl_attn_fwd_host,

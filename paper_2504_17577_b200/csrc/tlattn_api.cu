@@ -18,6 +18,7 @@
 #include "../../include/tlattn.h"
 #include "attn_fwd_sm100.cuh"
 #include "attn_fwd_sm100_2sm.cuh"
+#include "gemm_sm100_2sm.cuh"
 
 using namespace tlattn;
 
@@ -30,7 +31,7 @@ struct DeviceInfo {
   int sm_count = 0;
   int major = 0, minor = 0;
   bool ok = false;
-  bool smem_set[6] = {false, false, false, false, false, false};
+  bool smem_set[8] = {false, false, false, false, false, false, false, false};
 };
 
 constexpr int kMaxDevices = 64;
@@ -317,6 +318,76 @@ extern "C" int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_
   }
   g_last_launches = launches;
   return TL_OK;
+}
+
+// ------------------------------------------------------------------ GEMM
+namespace {
+bool encode_2d(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
+               int inner, int outer, unsigned box_inner, unsigned box_outer) {
+  // rank-4 map with two unit dimensions so the kernel shares the 4-D TMA instructions
+  const cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, 1, 1};
+  const cuuint64_t row = (cuuint64_t)inner * 2;
+  const cuuint64_t strides[3] = {row, row * (cuuint64_t)outer, row * (cuuint64_t)outer};
+  const cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+             4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool BF16>
+int launch_gemm(const GemmParams& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
+  auto kern = tl_gemm_kernel_2sm<BF16>;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di.smem_set[inst]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GCfg::SMEM_BYTES) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return TL_ERR_CUDA;
+      }
+      di.smem_set[inst] = true;
+    }
+  }
+  kern<<<2 * prm.tiles_m * prm.tiles_n, GCfg::THREADS, GCfg::SMEM_BYTES, stream>>>(prm);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  return TL_OK;
+}
+}  // namespace
+
+extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int K, int dtype,
+                       void* stream) {
+  g_last_launches = 0;
+  if (!a || !b || !c) return TL_ERR_INVALID_VALUE;
+  if (M < 1 || N < 1 || K < 1) return TL_ERR_INVALID_VALUE;
+  if (dtype != TL_DTYPE_F16 && dtype != TL_DTYPE_BF16) return TL_ERR_INVALID_VALUE;
+  if (N % 8 != 0 || K % 8 != 0) return TL_ERR_UNSUPPORTED;
+  auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0; };
+  if (!al(a) || !al(b) || !al(c)) return TL_ERR_UNSUPPORTED;
+  const long long tiles = (long long)((M + 255) / 256) * ((N + 255) / 256);
+  if (2 * tiles > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
+  int dev, rc;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  GemmParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (!encode_2d(enc, &prm.tm_a, a, dtype, K, M, 64, 128) ||
+      !encode_2d(enc, &prm.tm_b, b, dtype, N, K, 64, 64) ||
+      !encode_2d(enc, &prm.tm_c, c, dtype, N, M, 64, 128))
+    return TL_ERR_CUDA;
+  prm.M = M;
+  prm.N = N;
+  prm.K = K;
+  prm.tiles_m = (M + 255) / 256;
+  prm.tiles_n = (N + 255) / 256;
+  prm.group_n = 8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rc = dtype == TL_DTYPE_BF16 ? launch_gemm<true>(prm, *di, 6, st) : launch_gemm<false>(prm, *di, 7, st);
+  if (rc == TL_OK) g_last_launches = 1;
+  return rc;
 }
 
 extern "C" const char* tl_attn_strerror(int status) {

@@ -52,6 +52,8 @@ def load_library(path: str | None = None):
         lib.tl_attn_strerror.restype = ctypes.c_char_p
         lib.tl_attn_version.argtypes = []
         lib.tl_attn_version.restype = I
+        lib.tl_gemm.argtypes = [P, P, P, I, I, I, I, P]
+        lib.tl_gemm.restype = I
         lib.tl_attn_last_launch_count.argtypes = []
         lib.tl_attn_last_launch_count.restype = I
         _lib = lib
@@ -149,6 +151,25 @@ def attention(q, k, v, causal=False, scale=None, return_lse=True, out=None, lse_
     tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, int(bool(causal)), scale,
                 dtype_code(q.dtype), stream)
     return (o, lse) if return_lse else o
+
+
+def tl_gemm(a, b, c, M, N, K, dtype, stream=None):
+    """Direct mirror of the C entry point: C[M,N] = A[M,K] @ B[K,N]."""
+    _check(load_library().tl_gemm(_ptr(a), _ptr(b), _ptr(c), int(M), int(N), int(K), int(dtype),
+                                  _stream_handle(stream)))
+
+
+def gemm(a, b, out=None, stream=None):
+    """C = A @ B on the GPU for row-major fp16/bf16 A [M,K], B [K,N] (allocates C)."""
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0] or a.dtype != b.dtype:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "expected A[M,K], B[K,N] of one dtype")
+    if not (a.is_contiguous() and b.is_contiguous() and a.is_cuda):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "A and B must be contiguous CUDA tensors")
+    M, K = a.shape
+    N = b.shape[1]
+    c = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    tl_gemm(a, b, c, M, N, K, dtype_code(a.dtype), stream)
+    return c
 
 
 class HostAttention:
