@@ -343,6 +343,8 @@ def run_ours(args, world, rank, local):
             if name == cfg.name:
                 continue
             extra[name] = bench_one(CONFIGS[name], pk, steps=max(5, min(args.steps, 20)))
+        for gname in ("M5", "M2"):  # the paper's GEMM on Table 2 shapes
+            extra["gemm_" + gname] = bench_gemm(gname, pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -412,6 +414,41 @@ def bench_one(cfg, pk, steps=20, warmup=3):
     del q, k, v, o, lse
     torch.cuda.empty_cache()
     return res
+
+
+GEMM_TABLE2 = {"M2": (4096, 28672, 8192), "M5": (8192, 8192, 8192)}  # PAPER.md Table 2
+
+
+def bench_gemm(name, pk, iters=10):
+    """tl_gemm (bf16) on a Table 2 shape, with cuBLAS (torch.matmul) timed as context."""
+    from paper_2504_17577_b200 import gemm
+    from paper_2504_17577_b200.inputs import gen_tensor
+    M, N, K = GEMM_TABLE2[name]
+    a = gen_tensor((M, K), 2024, "q", torch.bfloat16, "cuda")
+    b = gen_tensor((K, N), 2024, "k", torch.bfloat16, "cuda")
+    c = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+
+    def med(fn):
+        for _ in range(3):
+            fn()
+        evs = []
+        for _ in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return float(np.median([x.elapsed_time(y) for x, y in evs]))
+
+    t = med(lambda: gemm(a, b, out=c))
+    tc = med(lambda: torch.matmul(a, b, out=c))
+    fl = 2.0 * M * N * K
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"shape": [M, N, K], "tflops": fl / t / 1e9, "kernel_ms": t,
+            "frac_of_peak": fl / t / 1e9 / pk["burst"], "cublas_tflops": fl / tc / 1e9,
+            "vs_cublas": tc / t}
 
 
 def main():
