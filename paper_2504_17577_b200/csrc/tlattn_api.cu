@@ -193,7 +193,9 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;
   const int unit_rows = pair ? KCfg2::UNIT_ROWS : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
-  prm.n_units = B * Hq * prm.n_mblk;
+  const long long units = (long long)B * Hq * prm.n_mblk;
+  if ((pair ? 2 * units : units) > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;  // grid.x limit
+  prm.n_units = static_cast<int>(units);
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
   prm.neg = scale < 0.f ? 1 : 0;
