@@ -91,8 +91,9 @@ int validate(const void* q, const void* k, const void* v, const void* o, const f
   if (!al(q, 16) || !al(k, 16) || !al(v, 16) || !al(o, 16)) return TL_ERR_UNSUPPORTED;
   if (lse && !al(lse, 4)) return TL_ERR_UNSUPPORTED;
   // grid.x = B * Hq * ceil(Sq/256) must fit in int32; TMA coordinates are int32
-  const long long units = (long long)B * Hq * ((Sq + 255) / 256);
-  if (units > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
+  const long long units = (long long)B * Hq * ((Sq + 255) / 256);       // single-CTA grid
+  const long long pair_grid = 2LL * B * Hq * ((Sq + 511) / 512);          // CTA-pair grid
+  if (units > 0x7fffffffLL || pair_grid > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
   return TL_OK;
 }
 
@@ -193,9 +194,7 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;
   const int unit_rows = pair ? KCfg2::UNIT_ROWS : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
-  const long long units = (long long)B * Hq * prm.n_mblk;
-  if ((pair ? 2 * units : units) > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;  // grid.x limit
-  prm.n_units = static_cast<int>(units);
+  prm.n_units = B * Hq * prm.n_mblk;  // bounded in validate()
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
   prm.neg = scale < 0.f ? 1 : 0;
