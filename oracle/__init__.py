@@ -15,6 +15,9 @@ from .oracle import (  # noqa: F401
     brute_force,
     gemm_rows,
     gemm_rows_parallel,
+    mla_decode,
+    mla_decode_parallel,
+    mla_brute,
     ORACLE_F16,
     ORACLE_BF16,
 )

@@ -60,6 +60,26 @@ int oracle_brute_force(const uint16_t* q, const uint16_t* k, const uint16_t* v, 
 int oracle_gemm_rows(const uint16_t* a, const uint16_t* b, int dtype, long M, long N, long K,
                      const long* rows, long nrows, double* c_out);
 
+/* MLA decode attention (Appendix B.3, Fig. 18), see mla_oracle.c.
+ * q[B][H][Dl], q_pe[B][H][Dr], kv[B][Skv][Hkv][Dl], k_pe[B][Skv][Hkv][Dr] (16-bit patterns),
+ * seqlens[B] (int32, each in [0, Skv]) or NULL (= Skv for every batch).
+ *   s_j  = scale * (q . kv_j + q_pe . k_pe_j),  j < n_b
+ *   o    = sum_j softmax(s)_j kv_j   (V = KV)   o_out [B][H][Dl]
+ *   lse  = log sum_j exp(s_j)                                    lse_out [B][H] or NULL
+ *   g    = h / (H / Hkv) */
+int oracle_mla_decode(const uint16_t* q, const uint16_t* q_pe, const uint16_t* kv,
+                      const uint16_t* k_pe, int dtype, const int32_t* seqlens, long B, long H,
+                      long Hkv, long Skv, long Dl, long Dr, double scale, double* o_out,
+                      double* lse_out);
+
+/* Independent explicit-matrix formulation for batch b (tiny shapes): concatenated
+ * operands, S materialised, P_hj = 1/sum_k exp(s_hk - s_hj), O = P KV. s_out/p_out are
+ * H x n_b (may be NULL), o_out H x Dl, lse_out H (may be NULL). */
+int oracle_mla_brute(const uint16_t* q, const uint16_t* q_pe, const uint16_t* kv,
+                     const uint16_t* k_pe, int dtype, const int32_t* seqlens, long B, long H,
+                     long Hkv, long Skv, long Dl, long Dr, double scale, long b, double* s_out,
+                     double* p_out, double* o_out, double* lse_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,8 @@ ORACLE_BF16 = 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRC = [os.path.join(_HERE, "attn_oracle.c"), os.path.join(_HERE, "gemm_oracle.c")]
+_SRC = [os.path.join(_HERE, "attn_oracle.c"), os.path.join(_HERE, "gemm_oracle.c"),
+        os.path.join(_HERE, "mla_oracle.c")]
 _lock = threading.Lock()
 _lib = None
 
@@ -56,6 +57,13 @@ def _load():
             lib.oracle_brute_force.restype = I
             lib.oracle_gemm_rows.argtypes = [P16, P16, I, L, L, L, PL, L, PD]
             lib.oracle_gemm_rows.restype = I
+            PI = ctypes.POINTER(ctypes.c_int32)
+            lib.oracle_mla_decode.argtypes = [P16, P16, P16, P16, I, PI, L, L, L, L, L, L, D,
+                                              PD, PD]
+            lib.oracle_mla_decode.restype = I
+            lib.oracle_mla_brute.argtypes = [P16, P16, P16, P16, I, PI, L, L, L, L, L, L, D, L,
+                                             PD, PD, PD, PD]
+            lib.oracle_mla_brute.restype = I
             _lib = lib
     return _lib
 
@@ -171,3 +179,69 @@ def gemm_rows_parallel(a, b, dtype, rows, threads=None):
         for k, r in enumerate(ch):
             out[pos[r]] = c[k]
     return out
+
+
+# --------------------------------------------------------------------------- MLA decode
+def _mla_dims(q, q_pe, kv, k_pe):
+    assert q.ndim == 3 and kv.ndim == 4 and q_pe.ndim == 3 and k_pe.ndim == 4
+    B, H, Dl = q.shape
+    Bk, Skv, Hkv, Dlk = kv.shape
+    Dr = q_pe.shape[2]
+    assert Bk == B and Dlk == Dl and q_pe.shape[:2] == (B, H)
+    assert k_pe.shape == (B, Skv, Hkv, Dr)
+    return B, H, Hkv, Skv, Dl, Dr
+
+
+def _pi32(a):
+    if a is None:
+        return None
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def mla_decode(q, q_pe, kv, k_pe, dtype, scale, seqlens=None):
+    """Fig. 18 MLA decode, plain fp64 definition: (o[B,H,Dl], lse[B,H])."""
+    lib = _load()
+    B, H, Hkv, Skv, Dl, Dr = _mla_dims(q, q_pe, kv, k_pe)
+    sl = None if seqlens is None else np.ascontiguousarray(np.asarray(seqlens, np.int32))
+    o = np.zeros((B, H, Dl), np.float64)
+    lse = np.zeros((B, H), np.float64)
+    rc = lib.oracle_mla_decode(_p16(q), _p16(q_pe), _p16(kv), _p16(k_pe), dtype, _pi32(sl),
+                               B, H, Hkv, Skv, Dl, Dr, float(scale), _pd(o), _pd(lse))
+    if rc != 0:
+        raise ValueError(f"oracle_mla_decode rejected its arguments (rc={rc})")
+    return o, lse
+
+
+def mla_decode_parallel(q, q_pe, kv, k_pe, dtype, scale, seqlens=None, batches=None,
+                        threads=None):
+    """mla_decode over independent batches on host threads; returns {b: (o[H,Dl], lse[H])}."""
+    B = q.shape[0]
+    batches = list(range(B)) if batches is None else list(batches)
+    sl = None if seqlens is None else np.asarray(seqlens, np.int32)
+
+    def one(b):
+        return b, mla_decode(q[b:b + 1], q_pe[b:b + 1], kv[b:b + 1], k_pe[b:b + 1], dtype,
+                             scale, None if sl is None else sl[b:b + 1])
+    threads = threads or len(os.sched_getaffinity(0))
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(one, batches))
+    return {b: (o[0], lse[0]) for b, (o, lse) in res}
+
+
+def mla_brute(q, q_pe, kv, k_pe, dtype, scale, b, seqlens=None):
+    """Explicit-matrix MLA for batch b: (S[H,n], P[H,n], O[H,Dl], lse[H])."""
+    lib = _load()
+    B, H, Hkv, Skv, Dl, Dr = _mla_dims(q, q_pe, kv, k_pe)
+    sl = None if seqlens is None else np.ascontiguousarray(np.asarray(seqlens, np.int32))
+    n = Skv if sl is None else int(sl[b])
+    S = np.zeros((H, n), np.float64)
+    P = np.zeros((H, n), np.float64)
+    O = np.zeros((H, Dl), np.float64)
+    lse = np.zeros((H,), np.float64)
+    rc = lib.oracle_mla_brute(_p16(q), _p16(q_pe), _p16(kv), _p16(k_pe), dtype, _pi32(sl),
+                              B, H, Hkv, Skv, Dl, Dr, float(scale), int(b),
+                              _pd(S), _pd(P), _pd(O), _pd(lse))
+    if rc != 0:
+        raise ValueError(f"oracle_mla_brute rejected its arguments (rc={rc})")
+    return S, P, O, lse

@@ -20,7 +20,7 @@ import math
 import numpy as np
 import torch
 
-TENSOR_ID = {"q": 1, "k": 2, "v": 3}
+TENSOR_ID = {"q": 1, "k": 2, "v": 3, "q_pe": 4, "kv": 5, "k_pe": 6, "seqlens": 7}
 _M32 = 0xFFFFFFFF
 
 
@@ -103,6 +103,25 @@ def gen_qkv(B, Hq, Hkv, Sq, Skv, D, dtype, seed, device, b_slice=None, hq_slice=
     v = gen_tensor((B, Skv, Hkv, D), seed, "v", dtype, device,
                    (bs, slice(0, Skv), hkv_slice or slice(0, Hkv), slice(0, D)))
     return q, k, v
+
+
+def gen_mla(B, H, Hkv, Skv, Dl, Dr, dtype, seed, device):
+    """MLA decode inputs (Fig. 18): q[B,H,Dl], q_pe[B,H,Dr],
+    kv[B,Skv,Hkv,Dl], k_pe[B,Skv,Hkv,Dr], iid N(0,1) rounded RN to ``dtype``."""
+    q = gen_tensor((B, H, Dl), seed, "q", dtype, device)
+    q_pe = gen_tensor((B, H, Dr), seed, "q_pe", dtype, device)
+    kv = gen_tensor((B, Skv, Hkv, Dl), seed, "kv", dtype, device)
+    k_pe = gen_tensor((B, Skv, Hkv, Dr), seed, "k_pe", dtype, device)
+    return q, q_pe, kv, k_pe
+
+
+def gen_seqlens(B, Skv, seed, lo=1):
+    """Ragged per-batch cache lengths, uniform integers in [lo, Skv] (int32 numpy),
+    from the same counter-based hash (reading M1)."""
+    key = _key(seed, TENSOR_ID["seqlens"])
+    h = _lowbias32(_lowbias32(torch.arange(B, dtype=torch.int64) ^ key))
+    span = Skv - lo + 1
+    return (lo + (h % span)).to(torch.int32).numpy()
 
 
 def to_bits(t: torch.Tensor) -> np.ndarray:
