@@ -118,14 +118,59 @@ uint64_t tl_attn_host_workspace_bytes(int B, int Hq, int Hkv, int Sq, int Skv, i
  */
 int tl_gemm(const void* a, const void* b, void* c, int M, int N, int K, int dtype, void* stream);
 
+/*
+ * tl_mla_decode — Multi-Head Latent Attention decode (PAPER.md Appendix
+ * B.3, Fig. 18 "FlashMLA"; benchmarked in Fig. 14), on the current
+ * device. One query token per (batch, head) attends to a latent KV cache:
+ *
+ *   n_b   = seqlens ? clamp(seqlens[b], 0, Skv) : Skv          (reading M1)
+ *   g     = h / (H / Hkv)                                         (cur_kv_head)
+ *   s_j   = scale * ( q[b,h,:] . kv[b,j,g,:] + q_pe[b,h,:] . k_pe[b,j,g,:] ),  j < n_b
+ *                                                 (two T.gemm into acc_s)
+ *   o[b,h,:]  = sum_j softmax_j(s) * kv[b,j,g,:]  (the value operand is KV itself)
+ *   lse[b,h]  = ln sum_j exp(s_j);   n_b = 0: o = 0, lse = -inf
+ *
+ *   q        device, [B][H][Dl]          contiguous, 16-byte aligned
+ *   q_pe     device, [B][H][Dr]
+ *   kv       device, [B][Skv][Hkv][Dl]   (Fig. 18 KV[batch, seqlen_kv, kv_head_num, dim])
+ *   k_pe     device, [B][Skv][Hkv][Dr]
+ *   o        device, [B][H][Dl], written in full
+ *   lse      device fp32 [B][H] (natural log), 4-byte aligned, or NULL
+ *   seqlens  device int32 [B] (per-batch cache lengths, clamped to [0, Skv] on the
+ *            device), or NULL (every batch has Skv keys)
+ *   Dl, Dr   must be 512 and 64 (the DeepSeek latent / rope dims of Fig. 18)
+ *   scale    natural-exp scale (callers normally pass 1/sqrt(Dl + Dr)); 0 / negative legal
+ *   dtype    TL_DTYPE_F16 or TL_DTYPE_BF16 for q, q_pe, kv, k_pe and o
+ *   ws       device workspace of ws_bytes >= tl_mla_decode_workspace_bytes(B, H, Hkv),
+ *            256-byte aligned; holds the split-KV partial results (contents scratch)
+ *   stream   cudaStream_t as void*
+ *
+ * Precision as tl_attn_fwd: fp32 scores and accumulators, fp32 l over unrounded p,
+ * P rounded RN to dtype before the PV product, O rounded RN. Split-KV pieces are merged in
+ * fp32. Three kernels per call (key-block prefix sums, decode, merge); stream-ordered, no
+ * allocation, graph-capturable. Ownership as tl_attn_fwd.
+ * Errors: TL_ERR_INVALID_VALUE (NULL q/q_pe/kv/k_pe/o/ws, size < 1, non-finite scale, bad
+ * dtype, workspace too small); TL_ERR_UNSUPPORTED (Dl != 512 or Dr != 64, H % Hkv != 0,
+ * misaligned pointer, sizes beyond 32-bit TMA coordinates, device not sm_100);
+ * TL_ERR_CUDA. Argument errors are returned before any CUDA call.
+ */
+int tl_mla_decode(const void* q, const void* q_pe, const void* kv, const void* k_pe, void* o,
+                  float* lse, const int* seqlens, int B, int H, int Hkv, int Skv, int Dl, int Dr,
+                  float scale, int dtype, void* ws, uint64_t ws_bytes, void* stream);
+
+/* Device workspace bytes tl_mla_decode needs on the CURRENT device (it depends on the SM
+ * count); 0 on bad arguments or when no device is available. */
+uint64_t tl_mla_decode_workspace_bytes(int B, int H, int Hkv);
+
 /* Static, NUL-terminated description of a tl_status code. Never NULL. */
 const char* tl_attn_strerror(int status);
 
 /* TLATTN_VERSION of the loaded library. */
 int tl_attn_version(void);
 
-/* Number of kernel launches the most recent successful tl_attn_fwd / tl_attn_fwd_host
- * call on this host thread issued (tl_attn_fwd: 1). For accounting in benchmarks. */
+/* Number of kernel launches the most recent successful tl_attn_fwd / tl_attn_fwd_host /
+ * tl_gemm / tl_mla_decode call on this host thread issued (tl_attn_fwd: 1,
+ * tl_mla_decode: 3). For accounting in benchmarks. */
 int tl_attn_last_launch_count(void);
 
 #ifdef __cplusplus

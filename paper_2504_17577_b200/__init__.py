@@ -16,6 +16,9 @@ from .tlattn import (  # noqa: F401
     attention,
     dtype_code,
     gemm,
+    mla_decode,
+    tl_mla_decode,
+    tl_mla_decode_workspace_bytes,
     tl_gemm,
     load_library,
     tl_attn_fwd,

@@ -78,3 +78,68 @@ CONFIGS = {
     "T0": AttnConfig("T0", 4, 32, 8, 8192, 8192, 128, torch.bfloat16, False, 1003,
                      "north_star target: D=128 non-causal S=8192 (C3 inputs, causal off)"),
 }
+
+
+# ------------------------------------------------------------------ MLA decode
+@dataclass(frozen=True)
+class MlaConfig:
+    """MLA decode workload (Fig. 18 / Fig. 14). The paper's Fig. 14 shapes are an
+    image; these are DeepSeek-V3-style decode shapes (latent 512 + rope 64, one kv head),
+    DESIGN.md "MLA workloads". ``ragged``: per-batch cache lengths uniform in [1, Skv]."""
+    name: str
+    B: int
+    H: int
+    Hkv: int
+    Skv: int
+    dtype: torch.dtype
+    ragged: bool
+    seed: int
+    Dl: int = 512
+    Dr: int = 64
+    note: str = ""
+
+    @property
+    def scale(self) -> float:
+        return 1.0 / math.sqrt(self.Dl + self.Dr)
+
+    @property
+    def torch_dtype(self) -> torch.dtype:
+        return self.dtype
+
+    @property
+    def dtype_name(self) -> str:
+        return {torch.float16: "f16", torch.bfloat16: "bf16"}[self.dtype]
+
+    def seqlens(self):
+        from .inputs import gen_seqlens
+        return gen_seqlens(self.B, self.Skv, self.seed) if self.ragged else None
+
+    def total_keys(self) -> int:
+        sl = self.seqlens()
+        return int(sl.sum()) if sl is not None else self.B * self.Skv
+
+    def flops(self) -> float:
+        """2*H*n*(Dl+Dr) for the scores + 2*H*n*Dl for P.V, summed over batches."""
+        return 2.0 * self.H * self.total_keys() * (2 * self.Dl + self.Dr)
+
+    def hbm_bytes(self) -> float:
+        """Algorithmic bytes: the latent cache (kv + k_pe) of every used key read once,
+        q / q_pe read, o written (16-bit), lse written (fp32)."""
+        e = 2
+        return (e * self.total_keys() * self.Hkv * (self.Dl + self.Dr)
+                + e * self.B * self.H * (2 * self.Dl + self.Dr) + 4 * self.B * self.H)
+
+    def as_dict(self):
+        return {"workload": self.name, "B": self.B, "H": self.H, "Hkv": self.Hkv,
+                "Skv": self.Skv, "Dl": self.Dl, "Dr": self.Dr, "dtype": self.dtype_name,
+                "ragged": self.ragged}
+
+
+MLA_CONFIGS = [
+    MlaConfig("MLA1", 64, 128, 1, 8192, torch.bfloat16, False, 2001,
+              note="DeepSeek-V3 decode, 128 heads (TP1), 8K cache"),
+    MlaConfig("MLA2", 128, 16, 1, 8192, torch.bfloat16, False, 2002,
+              note="16 heads per GPU (TP8), 8K cache"),
+    MlaConfig("MLA3", 32, 128, 1, 16384, torch.bfloat16, True, 2003,
+              note="ragged cache lengths uniform in [1, 16384]"),
+]

@@ -1,0 +1,680 @@
+// mla_decode_sm100.cuh — MLA decode attention for B200 (sm_100a), SURVEY §8(f) N1.
+//
+// What it computes: PAPER.md Appendix B.3, Fig. 18, see include/tlattn.h
+// tl_mla_decode: per (b, h) one query against the latent cache, scores
+// s_j = scale (q.kv_j + q_pe.kpe_j) (two T.gemm into acc_s), online softmax
+// (P:L660-679), O = softmax . KV (the value operand is KV_shared itself).
+//
+// B200 design. Fig. 18 tiles heads as the GEMM M dimension with a
+// [block_H x 512] fp32 accumulator in registers (Hopper wgmma). On sm_100 the accumulator
+// lives in TMEM: 128 heads x 512 fp32 would fill all 512 columns of an SM, leaving no room
+// for the score tile. So the tile is transposed — keys are the M dimension:
+//   S^T [128 keys x HC heads] = Khat [128 keys x 576] . Qhat^T      (tcgen05, TMEM)
+//   O^T [512 dv x HC heads]  += V^T  [512 x 128 keys] . P^T           (4 MMAs of M=128)
+// with HC = 32 query heads per CTA: TMEM = 2 x 32 (S^T double buffer) + 4 x 32 (O^T).
+// One thread per key row (TMEM lane) does the softmax; per-head (column) max and sum
+// are warp transposed-butterfly reductions plus a 4-warp smem step; l is kept as
+// per-thread partial sums and reduced once per segment.
+//
+//   warp 0     TMA producer: Qhat (8 x [32 heads x 64] + q_pe) once per segment, then
+//              Khat chunks [128 keys x 64 dims] (8 of KV + 1 of K_pe) and V units
+//              [64 keys x 128 dv] into ONE ring of 16 KB slots, in MMA consumption order
+//              (S(0), S(1), PV(0), S(2), PV(1), ...). V is re-read (from L2) for PV rather
+//              than kept resident: a 128-key block of Khat is 144 KB, so keeping it until
+//              its PV would leave no room to prefetch the next block.
+//   warp 1     MMA issuer (one thread): S(j+1) before PV(j), so the tensor core computes the
+//              next scores while the softmax of block j runs.
+//   warps 4-7  softmax + epilogue.
+// Work split (split-KV, the FlashDecoding / FlashMLA scheme; Fig. 18 has one CTA per
+// (batch, head block), which leaves most of 148 SMs idle at decode batch sizes): the key
+// blocks of all batches are concatenated (cum[] from tl_mla_meta_kernel) and each CTA of a
+// head tile takes an equal contiguous range; a range piece that covers a whole batch writes
+// O directly, partial pieces write fp32 (O, lse) to the workspace and tl_mla_combine_kernel
+// merges them.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "attn_fwd_sm100.cuh"  // pack2
+#include "ptx.cuh"
+
+namespace tlattn {
+namespace mla {
+
+constexpr int DL = 512;             // latent (kv_lora) dim, Fig. 18 `dim`
+constexpr int DR = 64;              // rope dim, Fig. 18 `pe_dim`
+constexpr int BLK = 128;            // keys per block (tcgen05 M of S^T)
+constexpr int HC = 32;              // query heads per CTA (tcgen05 N)
+constexpr int NKCH = DL / 64 + 1;   // Khat chunks per block: 8 of KV + 1 of K_pe
+constexpr int NVU = 8;              // V units per block: 4 dv chunks x 2 key halves
+constexpr int SLOT = 16384;         // ring slot: [128 keys x 64] or [2 x 64 keys x 64]
+constexpr int NSLOT = 10;
+constexpr int QCH = HC * 128;       // one [32 heads x 64] SW128 chunk of Qhat (4 KB)
+constexpr int PBYTES = BLK * HC * 2;  // P^T [128 keys x 32 heads] 16-bit, SW64 (8 KB)
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TM_S = 0;        // S^T buffers at columns 0, 32
+constexpr uint32_t TM_O = 64;       // O^T dv chunk m at columns 64 + 32 m
+constexpr float RESCALE_LOG2 = 8.0f;  // conditional rescale threshold (as the attention kernel)
+
+// Experiments only (WRONG results): 1 = no softmax arithmetic (P = raw S bits),
+// 3 = no V loads / PV MMAs (K stream + softmax alone).
+#ifndef TLATTN_MLA_EXP
+#define TLATTN_MLA_EXP 0
+#endif
+
+constexpr int OFF_RING = 0;
+constexpr int OFF_Q = OFF_RING + NSLOT * SLOT;
+constexpr int OFF_P = OFF_Q + NKCH * QCH;
+constexpr int OFF_RED = OFF_P + 2 * PBYTES;        // float red[2][4][32] + redl[4][32]
+constexpr int OFF_BAR = OFF_RED + 3 * 4 * 32 * 4;
+// ring_full[NSLOT], ring_empty[NSLOT], q_full, q_empty, s_full[2], s_free[2], p_full[2],
+// o_done[2], o_free
+constexpr int NUM_BARS = 2 * NSLOT + 11;
+constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+constexpr int SMEM_USED = OFF_TMEMPTR + 16;
+constexpr int SMEM_BYTES = SMEM_USED + 1024;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+
+struct MlaParams {
+  CUtensorMap tm_q;    // q   [B][H][DL]       as (DL, H, 1, B),   box (64, 32, 1, 1)
+  CUtensorMap tm_qpe;  // q_pe[B][H][DR]       as (DR, H, 1, B),   box (64, 32, 1, 1)
+  CUtensorMap tm_k;    // kv  [B][Skv][Hkv][DL] as (DL, Hkv, Skv, B), box (64, 1, 128, 1)
+  CUtensorMap tm_v;    // kv, box (64, 1, 64, 1)
+  CUtensorMap tm_kpe;  // k_pe[B][Skv][Hkv][DR], box (64, 1, 128, 1)
+  void* o;             // [B][H][DL]
+  float* lse;          // [B][H] natural log, or nullptr
+  const int* seqlens;  // [B] or nullptr (= Skv)
+  int* cum;            // workspace: [B+1] prefix sums of key blocks per batch
+  float* ws_o;         // workspace: [NHG][P][2][HC][DL] partial O (normalised)
+  float* ws_lse;       // workspace: [NHG][P][2][HC] partial lse (log2 units)
+  int B, H, Hkv, Skv;
+  int g;               // H / Hkv (query heads per kv head)
+  int T;               // head tiles per kv head = ceil(g / HC)
+  int P;               // partitions (CTAs) per head tile
+  int CL;              // cluster size: CL head tiles of one kv head share every K/V load
+                       // (TMA multicast); 1, 2 or 4, divides T
+  float c_log2;        // |scale| log2(e)
+  int neg;             // scale < 0: negate Qhat (B operand) in the S^T descriptor
+};
+
+__device__ __forceinline__ int seq_len(const MlaParams& p, int b) {
+  if (p.seqlens == nullptr) return p.Skv;
+  const int n = p.seqlens[b];
+  return n < 0 ? 0 : (n > p.Skv ? p.Skv : n);  // documented clamp (tlattn.h)
+}
+
+__device__ __forceinline__ long long part_start(int part, long long W, int P) {
+  return (long long)part * W / P;
+}
+
+// last batch b with cum[b] <= s (and a non-empty key range when s < W)
+__device__ __forceinline__ int batch_of(const int* cum, int B, long long s) {
+  int lo = 0, hi = B;  // answer in [0, B)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((long long)cum[mid] <= s) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One piece of a partition's block range that lies in one batch.
+struct Seg {
+  int b, k0, n;   // batch, first block (within the batch), number of blocks
+  int len;        // keys of batch b
+  bool partial;   // does not cover the whole batch -> workspace
+  int slot;       // workspace slot (0 = first piece of the partition, 1 = later)
+};
+
+// Iterates the pieces of partition `part` (same sequence in every role).
+struct SegIter {
+  long long s, e;
+  int b;
+  bool first;
+  __device__ __forceinline__ SegIter(const MlaParams& p, int part) {
+    const long long W = p.cum[p.B];
+    s = part_start(part, W, p.P);
+    e = part_start(part + 1, W, p.P);
+    b = (s < e) ? batch_of(p.cum, p.B, s) : 0;
+    first = true;
+  }
+  __device__ __forceinline__ bool next(const MlaParams& p, Seg& sg) {
+    if (s >= e) return false;
+    const long long c0 = p.cum[b], c1 = p.cum[b + 1];
+    const long long stop = e < c1 ? e : c1;
+    sg.b = b;
+    sg.k0 = (int)(s - c0);
+    sg.n = (int)(stop - s);
+    sg.len = seq_len(p, b);
+    sg.partial = !(s == c0 && stop == c1);
+    sg.slot = first ? 0 : 1;
+    first = false;
+    s = stop;
+    ++b;
+    while (s < e && b < p.B && (long long)p.cum[b + 1] <= s) ++b;  // skip empty batches
+    return true;
+  }
+};
+
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                               uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(layout) << 61;  // 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+  return d;
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_constant__ MlaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_u32);
+  const uint32_t sRing = base + OFF_RING;
+  const uint32_t sQ = base + OFF_Q;
+  const uint32_t sP = base + OFF_P;
+  float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][32]
+  float* redl = red + 2 * 4 * 32;                          // [4][32]
+  const uint32_t bar0 = base + OFF_BAR;
+  auto bar_full = [&](int s) { return bar0 + 8u * s; };
+  auto bar_empty = [&](int s) { return bar0 + 8u * (NSLOT + s); };
+  const uint32_t bar_q_full = bar0 + 8u * (2 * NSLOT);
+  const uint32_t bar_q_empty = bar_q_full + 8u;
+  auto bar_s_full = [&](int i) { return bar0 + 8u * (2 * NSLOT + 2 + i); };
+  auto bar_s_free = [&](int i) { return bar0 + 8u * (2 * NSLOT + 4 + i); };
+  auto bar_p_full = [&](int i) { return bar0 + 8u * (2 * NSLOT + 6 + i); };
+  auto bar_o_done = [&](int i) { return bar0 + 8u * (2 * NSLOT + 8 + i); };
+  const uint32_t bar_o_free = bar0 + 8u * (2 * NSLOT + 10);
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + OFF_TMEMPTR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // cluster = CL head tiles of one kv head over the same partition of the key blocks
+  const uint32_t rank = p.CL > 1 ? cluster_ctarank() : 0u;
+  const int cid = blockIdx.x / p.CL;
+  const int part = cid % p.P;
+  const int hgi = (cid / p.P) * p.CL + rank;  // head tile id = kvh * T + t
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << p.CL) - 1u);
+  const int kvh = hgi / p.T;
+  const int t = hgi % p.T;
+  const int h0 = kvh * p.g + t * HC;             // first query head of this tile
+  const int nvalid = min(HC, p.g - t * HC);      // heads of this tile inside the kv group
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_q);
+    prefetch_tmap(&p.tm_qpe);
+    prefetch_tmap(&p.tm_k);
+    prefetch_tmap(&p.tm_v);
+    prefetch_tmap(&p.tm_kpe);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_empty(s), p.CL);  // released by the MMA of every CTA of the cluster
+    }
+    mbar_init(bar_q_full, 1);
+    mbar_init(bar_q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_s_full(i), 1);
+      mbar_init(bar_s_free(i), 4);
+      mbar_init(bar_p_full(i), 4);
+      mbar_init(bar_o_done(i), 1);
+    }
+    mbar_init(bar_o_free, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_ptr_smem));
+  tc_fence_before();
+  if (p.CL > 1) cluster_sync();  // peers' barriers initialised before any multicast / remote arrive
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_smem;
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    // Ring slots are filled by multicast: unit `it` is loaded by CTA (it % CL) into the same
+    // slot of every CTA of the cluster; a slot is refilled only after all CL MMAs released it.
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_k = policy_evict_last();   // re-read as V and by the other head tiles
+      const uint64_t pol_v = policy_evict_last();
+      uint32_t it = 0;
+      int nseg = 0;
+      SegIter si(p, part);
+      Seg sg;
+      bool mine = true;  // this CTA issues the current unit's load
+      auto acquire = [&](uint32_t& slot_addr) -> uint32_t {
+        const int slot = it % NSLOT;
+        if (it >= (uint32_t)NSLOT) mbar_wait(bar_empty(slot), ((it / NSLOT) - 1) & 1);
+        mbar_arrive_expect_tx(bar_full(slot), SLOT);
+        slot_addr = sRing + slot * SLOT;
+        mine = (it % p.CL) == rank;
+        ++it;
+        return bar_full(slot);
+      };
+      auto load = [&](uint32_t dst, const CUtensorMap* m, uint32_t fb, int c0, int c1, int c2, int c3,
+                      uint64_t pol) {
+        if (!mine) return;
+        if (p.CL > 1) tma_load_4d_mc(dst, m, fb, c0, c1, c2, c3, mc_mask, pol);
+        else tma_load_4d(dst, m, fb, c0, c1, c2, c3, pol);
+      };
+      while (si.next(p, sg)) {
+        if (nseg > 0) mbar_wait(bar_q_empty, (nseg - 1) & 1);  // previous segment's S MMAs done
+        mbar_arrive_expect_tx(bar_q_full, NKCH * QCH);
+#pragma unroll 1
+        for (int c = 0; c < DL / 64; ++c)
+          tma_load_4d(sQ + c * QCH, &p.tm_q, bar_q_full, c * 64, h0, 0, sg.b, pol_q);
+        tma_load_4d(sQ + (DL / 64) * QCH, &p.tm_qpe, bar_q_full, 0, h0, 0, sg.b, pol_q);
+#pragma unroll 1
+        for (int jj = 0; jj <= sg.n; ++jj) {
+          if (jj < sg.n) {  // Khat(j): 8 KV chunks + K_pe
+            const int key0 = (sg.k0 + jj) * BLK;
+#pragma unroll 1
+            for (int c = 0; c < NKCH; ++c) {
+              uint32_t dst;
+              const uint32_t fb = acquire(dst);
+              if (c < DL / 64) load(dst, &p.tm_k, fb, c * 64, kvh, key0, sg.b, pol_k);
+              else load(dst, &p.tm_kpe, fb, 0, kvh, key0, sg.b, pol_k);
+            }
+          }
+          if (jj >= 1 && TLATTN_MLA_EXP != 3) {  // V(j-1): unit u = dv chunk (u>>1), key half (u&1)
+            const int key0 = (sg.k0 + jj - 1) * BLK;
+#pragma unroll 1
+            for (int u = 0; u < NVU; ++u) {
+              uint32_t dst;
+              const uint32_t fb = acquire(dst);
+              const int m = u >> 1, hf = u & 1;
+              load(dst, &p.tm_v, fb, (2 * m) * 64, kvh, key0 + hf * 64, sg.b, pol_v);
+              load(dst + SLOT / 2, &p.tm_v, fb, (2 * m + 1) * 64, kvh, key0 + hf * 64, sg.b, pol_v);
+            }
+          }
+        }
+        ++nseg;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    if (lane == 0) {
+      constexpr uint32_t FMT = BF16 ? 1u : 0u;
+      // S^T = Khat Qhat^T: A = Khat (K-major), B = Qhat (K-major), M=128 keys, N=HC heads
+      const uint32_t IDESC_S = make_idesc_f16(FMT, BLK, HC, 0, 0, 0) | ((p.neg ? 1u : 0u) << 14);
+      // O^T += V^T P^T: A = V^T (MN-major: dv contiguous), B = P^T (MN-major: heads
+      // contiguous), M=128 dv, N=HC heads
+      constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, 128, HC, 1, 1, 0);
+      uint32_t it = 0;
+      uint32_t gb = 0;  // global block counter (S / P buffer phases)
+      int nseg = 0;
+      SegIter si(p, part);
+      Seg sg;
+      auto wait_slot = [&]() -> uint32_t {
+        const int slot = it % NSLOT;
+        mbar_wait(bar_full(slot), (it / NSLOT) & 1);
+        tc_fence_after();
+        return slot;
+      };
+      while (si.next(p, sg)) {
+        mbar_wait(bar_q_full, nseg & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int jj = 0; jj <= sg.n; ++jj) {
+          if (jj < sg.n) {  // S(gb + jj)
+            const uint32_t gs = gb + jj;
+            const uint32_t sb = gs & 1;
+            if (gs >= 2) mbar_wait(bar_s_free(sb), ((gs - 2) >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < NKCH; ++c) {
+              const int slot = wait_slot();
+              const uint32_t a0 = sRing + slot * SLOT;
+              const uint32_t b0 = sQ + c * QCH;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_f16_ss(tmem_base + TM_S + sb * HC, make_sdesc(a0 + kk * 32, 16, 1024, 2),
+                           make_sdesc(b0 + kk * 32, 16, 1024, 2), IDESC_S, (c | kk) ? 1u : 0u);
+              if (p.CL > 1) mma_commit_mc(bar_empty(slot), mc_mask);
+              else mma_commit(bar_empty(slot));
+              ++it;
+            }
+            mma_commit(bar_s_full(sb));
+            if (jj == sg.n - 1) mma_commit(bar_q_empty);
+          }
+          if (jj >= 1) {  // PV(gb + jj - 1)
+            const uint32_t gp = gb + jj - 1;
+            const uint32_t pb = gp & 1;
+            if (jj == 1 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
+            mbar_wait(bar_p_full(pb), (gp >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int u = 0; u < (TLATTN_MLA_EXP == 3 ? 0 : NVU); ++u) {
+              const int m = u >> 1, hf = u & 1;
+              const int slot = wait_slot();
+              const uint32_t a0 = sRing + slot * SLOT;
+              const uint32_t b0 = sP + pb * PBYTES + hf * (64 * 64);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                // A: V^T MN-major SW128, 16 keys = 16 rows of 128 B; LBO = 8 KB to the next
+                // 64-wide dv atom. B: P^T MN-major SW64, 16 keys = 16 rows of 64 B.
+                mma_f16_ss(tmem_base + TM_O + m * HC, make_sdesc(a0 + kk * 2048, SLOT / 2, 1024, 2),
+                           make_sdesc(b0 + kk * 1024, 4096, 512, 4), IDESC_PV,
+                           (jj > 1 || hf > 0 || kk > 0) ? 1u : 0u);
+              }
+              if (p.CL > 1) mma_commit_mc(bar_empty(slot), mc_mask);
+              else mma_commit(bar_empty(slot));
+              ++it;
+            }
+            mma_commit(bar_o_done(pb));
+          }
+        }
+        gb += sg.n;
+        ++nseg;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ============================ softmax + epilogue ============================
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;  // key within the block == TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const float c = p.c_log2;
+    const unsigned FULL = 0xffffffffu;
+    uint32_t gb = 0;
+    int nseg = 0;
+    SegIter si(p, part);
+    Seg sg;
+    while (si.next(p, sg)) {
+      float m = -INFINITY;  // running max (log2 units) of head `lane` (same in all 4 warps)
+      float lpart[HC];      // this key-thread's share of l for every head
+#pragma unroll
+      for (int h = 0; h < HC; ++h) lpart[h] = 0.f;
+#pragma unroll 1
+      for (int jj = 0; jj < sg.n; ++jj) {
+        const uint32_t gs = gb + jj;
+        const uint32_t sb = gs & 1;
+        mbar_wait(bar_s_full(sb), (gs >> 1) & 1);
+        tc_fence_after();
+        float s[HC];
+        tmem_ld32(tmem_base + lane_off + TM_S + sb * HC, *reinterpret_cast<uint32_t(*)[32]>(s));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_s_free(sb));
+        uint32_t pk[HC / 2];
+        bool resc = false;
+        float m_new = m;
+        float alpha = 1.f;
+        if constexpr (TLATTN_MLA_EXP == 1) {
+#pragma unroll
+          for (int h = 0; h < HC / 2; ++h) pk[h] = __float_as_uint(s[2 * h]);
+        } else {
+        // tail mask: keys >= len of this batch do not take part (TMA zero-fills beyond Skv)
+        if ((sg.k0 + jj) * BLK + row >= sg.len) {
+#pragma unroll
+          for (int h = 0; h < HC; ++h) s[h] = -INFINITY;
+        }
+        // per-head (column) max over the 128 keys: transposed butterfly inside the warp
+        // (lane l ends with column l), then the 4 warps through smem (T.reduce_max)
+        float v[HC];
+#pragma unroll
+        for (int h = 0; h < HC; ++h) v[h] = s[h];
+#pragma unroll
+        for (int w = HC / 2; w >= 1; w >>= 1) {
+          const bool up = (lane & w) != 0;
+#pragma unroll
+          for (int i = 0; i < w; ++i) {
+            const float send = up ? v[i] : v[i + w];
+            const float keep = up ? v[i + w] : v[i];
+            v[i] = fmaxf(keep, __shfl_xor_sync(FULL, send, w));
+          }
+        }
+        float* rb = red + (gs & 1) * 128;
+        rb[q4 * 32 + lane] = v[0];
+        named_bar_sync(1, 128);
+        const float mx = fmaxf(fmaxf(rb[lane], rb[32 + lane]), fmaxf(rb[64 + lane], rb[96 + lane]));
+        const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
+        m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        alpha = ex2(m - m_use);  // scores_scale; 0 on the first block
+        // p = exp2(s c - m_head), l partial sums from the unrounded p (R8)
+        resc = __any_sync(FULL, alpha != 1.f);
+#pragma unroll
+        for (int h = 0; h < HC; h += 2) {
+          const float m0 = __shfl_sync(FULL, m_use, h);
+          const float m1 = __shfl_sync(FULL, m_use, h + 1);
+          const float p0 = ex2(fmaf(s[h], c, -m0));
+          const float p1 = ex2(fmaf(s[h + 1], c, -m1));
+          if (resc) {
+            lpart[h] *= __shfl_sync(FULL, alpha, h);
+            lpart[h + 1] *= __shfl_sync(FULL, alpha, h + 1);
+          }
+          lpart[h] += p0;
+          lpart[h + 1] += p1;
+          pk[h / 2] = pack2<BF16>(p0, p1);  // P rounded RN to the dtype (S_shared)
+        }
+        }
+        // P^T buffer sb is free once PV(gs-2) completed
+        if (gs >= 2) mbar_wait(bar_o_done(sb), ((gs - 2) >> 1) & 1);
+        if (resc && jj > 0) {
+          // acc_o *= scores_scale: O^T columns are heads; needs PV(gs-1) done
+          mbar_wait(bar_o_done(sb ^ 1), ((gs - 1) >> 1) & 1);
+          tc_fence_after();
+          float al[HC];
+#pragma unroll
+          for (int h = 0; h < HC; ++h) al[h] = __shfl_sync(FULL, alpha, h);
+#pragma unroll 1
+          for (int mm = 0; mm < DL / 128; ++mm) {
+            uint32_t ov[32];
+            tmem_ld32(tmem_base + lane_off + TM_O + mm * HC, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int h = 0; h < HC; ++h) ov[h] = __float_as_uint(__uint_as_float(ov[h]) * al[h]);
+            tmem_st32(tmem_base + lane_off + TM_O + mm * HC, ov);
+          }
+          tmem_st_wait();
+        }
+        // P^T row (this key, 32 heads = 64 B) -> smem, MN-major SWIZZLE_64B:
+        // 16-B unit u of row r lands at u ^ ((r >> 1) & 3)
+        const uint32_t prow = sP + sb * PBYTES + row * 64;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          st_shared_v4(prow + ((u ^ ((row >> 1) & 3)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
+                       pk[4 * u + 3]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_p_full(sb));
+        m = m_new;
+      }
+      // ---- epilogue: l = sum of the partial sums, O = O^T / l, LSE
+      const uint32_t glast = gb + sg.n - 1;
+      mbar_wait(bar_o_done(glast & 1), (glast >> 1) & 1);
+      tc_fence_after();
+      {
+        float v[HC];
+#pragma unroll
+        for (int h = 0; h < HC; ++h) v[h] = lpart[h];
+#pragma unroll
+        for (int w = HC / 2; w >= 1; w >>= 1) {
+          const bool up = (lane & w) != 0;
+#pragma unroll
+          for (int i = 0; i < w; ++i) {
+            const float send = up ? v[i] : v[i + w];
+            const float keep = up ? v[i + w] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, w);
+          }
+        }
+        redl[q4 * 32 + lane] = v[0];
+      }
+      named_bar_sync(1, 128);
+      const float L = (redl[lane] + redl[32 + lane]) + (redl[64 + lane] + redl[96 + lane]);
+      const float m_fin = (m == -INFINITY) ? 0.f : m;
+      const float inv = (L > 0.f) ? 1.f / L : 0.f;
+      const float lse2 = (L > 0.f) ? m_fin + __log2f(L) : -INFINITY;
+      float iv[HC];
+#pragma unroll
+      for (int h = 0; h < HC; ++h) iv[h] = __shfl_sync(FULL, inv, h);
+      const size_t wslot = ((size_t)(hgi * p.P + part) * 2 + sg.slot);
+#pragma unroll 1
+      for (int mm = 0; mm < DL / 128; ++mm) {
+        uint32_t ov[32];
+        tmem_ld32(tmem_base + lane_off + TM_O + mm * HC, ov);
+        tmem_ld_wait();
+        const int dv = mm * 128 + row;
+        if (!sg.partial) {
+          using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+          T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)sg.b * p.H + h0) * DL + dv;
+#pragma unroll
+          for (int h = 0; h < HC; ++h) {
+            if (h < nvalid) {
+              const float x = __uint_as_float(ov[h]) * iv[h];
+              if constexpr (BF16) ob[(size_t)h * DL] = __float2bfloat16_rn(x);
+              else ob[(size_t)h * DL] = __float2half_rn(x);
+            }
+          }
+        } else {
+          float* wo = p.ws_o + wslot * HC * DL + dv;
+#pragma unroll
+          for (int h = 0; h < HC; ++h) wo[(size_t)h * DL] = __uint_as_float(ov[h]) * iv[h];
+        }
+      }
+      if (q4 == 0) {
+        if (!sg.partial) {
+          if (p.lse != nullptr && lane < nvalid)
+            p.lse[(size_t)sg.b * p.H + h0 + lane] = lse2 * 0.69314718055994531f;
+        } else {
+          p.ws_lse[wslot * HC + lane] = lse2;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_o_free);
+      gb += sg.n;
+      ++nseg;
+    }
+  }
+
+  // every MMA of this CTA has completed (softmax waited the last PV), so all its multicast
+  // releases have landed in the peers; no CTA leaves while a peer may still signal it
+  if (p.CL > 1) cluster_sync();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// cum[b] = sum_{b' < b} ceil(len_b' / BLK), cum[B] = W. One CTA, chunked block scan.
+__global__ void __launch_bounds__(1024) tl_mla_meta_kernel(const int* seqlens, int B, int Skv, int* cum) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base0 = 0; base0 < B; base0 += 1024) {
+    const int b = base0 + threadIdx.x;
+    int n = 0;
+    if (b < B) {
+      int len = seqlens ? seqlens[b] : Skv;
+      len = len < 0 ? 0 : (len > Skv ? Skv : len);
+      n = (len + BLK - 1) / BLK;
+    }
+    int x = n;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0) + x - n;
+    if (b < B) cum[b] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + n;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cum[B] = carry;
+}
+
+// Merge the partial (O, lse) pieces of split batches; write zeros / -inf for empty ones.
+// Grid: (B, Hkv * T); 256 threads: warp w handles heads w, w+8, w+16, w+24 of the tile.
+template <bool BF16>
+__global__ void __launch_bounds__(256) tl_mla_combine_kernel(const __grid_constant__ MlaParams p) {
+  const int b = blockIdx.x;
+  const int hgi = blockIdx.y;
+  const int kvh = hgi / p.T, t = hgi % p.T;
+  const int h0 = kvh * p.g + t * HC;
+  const int nvalid = min(HC, p.g - t * HC);
+  const long long W = p.cum[p.B];
+  const long long c0 = p.cum[b], c1 = p.cum[b + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+  T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)b * p.H + h0) * DL;
+  if (c1 == c0) {  // no keys (seqlens[b] == 0): O = 0, LSE = -inf (reading M1 / R4)
+    for (int h = warp; h < nvalid; h += 8) {
+      for (int d = lane; d < DL; d += 32) {
+        if constexpr (BF16) ob[(size_t)h * DL + d] = __float2bfloat16_rn(0.f);
+        else ob[(size_t)h * DL + d] = __float2half_rn(0.f);
+      }
+      if (p.lse != nullptr && lane == 0) p.lse[(size_t)b * p.H + h0 + h] = -INFINITY;
+    }
+    return;
+  }
+  // partitions covering [c0, c1): p_lo = last with start <= c0, p_hi = last with start <= c1-1
+  auto last_start_le = [&](long long x) {
+    int q = (int)((x * p.P) / W);
+    while (q + 1 < p.P && part_start(q + 1, W, p.P) <= x) ++q;
+    while (q > 0 && part_start(q, W, p.P) > x) --q;
+    return q;
+  };
+  const int p_lo = last_start_le(c0), p_hi = last_start_le(c1 - 1);
+  if (p_lo == p_hi) return;  // one piece: the decode kernel wrote O / LSE directly
+  for (int h = warp; h < nvalid; h += 8) {
+    float mx = -INFINITY;
+    for (int q = p_lo; q <= p_hi; ++q) {
+      if (part_start(q, W, p.P) == part_start(q + 1, W, p.P)) continue;  // empty partition
+      const int slot = (part_start(q, W, p.P) >= c0) ? 0 : 1;
+      mx = fmaxf(mx, p.ws_lse[((size_t)(hgi * p.P + q) * 2 + slot) * HC + h]);
+    }
+    float acc[DL / 32];
+#pragma unroll
+    for (int i = 0; i < DL / 32; ++i) acc[i] = 0.f;
+    float L = 0.f;
+    for (int q = p_lo; q <= p_hi; ++q) {
+      if (part_start(q, W, p.P) == part_start(q + 1, W, p.P)) continue;
+      const int slot = (part_start(q, W, p.P) >= c0) ? 0 : 1;
+      const size_t ws = (size_t)(hgi * p.P + q) * 2 + slot;
+      const float w = ex2(p.ws_lse[ws * HC + h] - mx);
+      L += w;
+      const float* src = p.ws_o + (ws * HC + h) * DL;
+#pragma unroll
+      for (int i = 0; i < DL / 32; ++i) acc[i] = fmaf(w, src[i * 32 + lane], acc[i]);
+    }
+    const float inv = 1.f / L;
+#pragma unroll
+    for (int i = 0; i < DL / 32; ++i) {
+      if constexpr (BF16) ob[(size_t)h * DL + i * 32 + lane] = __float2bfloat16_rn(acc[i] * inv);
+      else ob[(size_t)h * DL + i * 32 + lane] = __float2half_rn(acc[i] * inv);
+    }
+    if (p.lse != nullptr && lane == 0)
+      p.lse[(size_t)b * p.H + h0 + h] = (mx + __log2f(L)) * 0.69314718055994531f;
+  }
+}
+
+}  // namespace mla
+}  // namespace tlattn

@@ -19,6 +19,7 @@
 #include "attn_fwd_sm100.cuh"
 #include "attn_fwd_sm100_2sm.cuh"
 #include "gemm_sm100_2sm.cuh"
+#include "mla_decode_sm100.cuh"
 
 using namespace tlattn;
 
@@ -31,7 +32,7 @@ struct DeviceInfo {
   int sm_count = 0;
   int major = 0, minor = 0;
   bool ok = false;
-  bool smem_set[8] = {false, false, false, false, false, false, false, false};
+  bool smem_set[16] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -388,6 +389,194 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   rc = dtype == TL_DTYPE_BF16 ? launch_gemm<true>(prm, *di, 6, st) : launch_gemm<false>(prm, *di, 7, st);
   if (rc == TL_OK) g_last_launches = 1;
+  return rc;
+}
+
+// ------------------------------------------------------------------ MLA decode
+namespace {
+struct MlaPlan {
+  int T, NHG, P, CL;
+  size_t off_lse, off_o, bytes;
+};
+
+int mla_cluster_size(int T) {
+  if (const char* e = std::getenv("TLATTN_MLA_CL")) {  // A/B experiments only
+    const int v = std::atoi(e);
+    if ((v == 1 || v == 2 || v == 4) && T % v == 0) return v;
+  }
+  // measured on B200: multicast clusters ran slower than independent CTAs
+  // (lockstep ring, no L2 relief at cluster size <= 4), so the default is 1
+  (void)T;
+  return 1;
+}
+
+// Clusters of `cl` MLA CTAs that fit on the device at once (cached per device and size).
+int mla_max_clusters(int dev, int cl, int sm_count);
+
+MlaPlan plan_mla(int B, int H, int Hkv, int dev, int sm_count) {
+  MlaPlan pl;
+  const int g = H / Hkv;
+  pl.T = (g + mla::HC - 1) / mla::HC;
+  pl.NHG = Hkv * pl.T;
+  pl.CL = mla_cluster_size(pl.T);
+  // all CTAs co-resident (one per SM): clusters that fit / cluster groups = partitions
+  const int groups = pl.NHG / pl.CL;
+  pl.P = mla_max_clusters(dev, pl.CL, sm_count) / groups;
+  if (pl.P < 1) pl.P = 1;
+  pl.off_lse = al256((size_t)(B + 1) * 4);
+  pl.off_o = pl.off_lse + al256((size_t)pl.NHG * pl.P * 2 * mla::HC * 4);
+  pl.bytes = pl.off_o + (size_t)pl.NHG * pl.P * 2 * mla::HC * mla::DL * 4;
+  return pl;
+}
+
+bool encode_4d(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
+               const cuuint64_t (&dims)[4], const cuuint32_t (&box)[4]) {
+  const cuuint64_t strides[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+             4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+std::mutex g_mla_mu;
+int g_mla_clusters[kMaxDevices][5] = {};
+
+bool mla_smem_attr(int dev) {
+  static bool done[kMaxDevices] = {};
+  if (done[dev]) return true;
+  if (cudaFuncSetAttribute(mla::tl_mla_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           mla::SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           mla::SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  done[dev] = true;
+  return true;
+}
+
+int mla_max_clusters(int dev, int cl, int sm_count) {
+  std::lock_guard<std::mutex> lk(g_mla_mu);
+  if (g_mla_clusters[dev][cl] > 0) return g_mla_clusters[dev][cl];
+  int n = sm_count / cl;
+  if (mla_smem_attr(dev)) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl * (sm_count / cl), 1, 1);
+    cfg.blockDim = dim3(mla::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = mla::SMEM_BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, mla::tl_mla_decode_kernel<true>, &cfg) == cudaSuccess && c > 0)
+      n = c;
+    cudaGetLastError();
+  }
+  g_mla_clusters[dev][cl] = n;
+  return n;
+}
+
+template <bool BF16>
+int launch_mla(const mla::MlaParams& prm, int dev, int B, const int* seqlens, int Skv,
+               cudaStream_t stream) {
+  {
+    std::lock_guard<std::mutex> lk(g_mla_mu);
+    if (!mla_smem_attr(dev)) return TL_ERR_CUDA;
+  }
+  mla::tl_mla_meta_kernel<<<1, 1024, 0, stream>>>(seqlens, B, Skv, prm.cum);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(prm.Hkv * prm.T * prm.P, 1, 1);
+  cfg.blockDim = dim3(mla::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = mla::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = prm.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, mla::tl_mla_decode_kernel<BF16>, prm) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  mla::tl_mla_combine_kernel<BF16><<<dim3(B, prm.Hkv * prm.T), 256, 0, stream>>>(prm);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  return TL_OK;
+}
+}  // namespace
+
+extern "C" uint64_t tl_mla_decode_workspace_bytes(int B, int H, int Hkv) {
+  if (B < 1 || H < 1 || Hkv < 1 || H % Hkv != 0) return 0;
+  int dev;
+  DeviceInfo* di;
+  if (current_device(&dev, &di) != TL_OK) return 0;
+  return plan_mla(B, H, Hkv, dev, di->sm_count).bytes;
+}
+
+extern "C" int tl_mla_decode(const void* q, const void* q_pe, const void* kv, const void* k_pe,
+                             void* o, float* lse, const int* seqlens, int B, int H, int Hkv,
+                             int Skv, int Dl, int Dr, float scale, int dtype, void* ws,
+                             uint64_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (!q || !q_pe || !kv || !k_pe || !o || !ws) return TL_ERR_INVALID_VALUE;
+  if (B < 1 || H < 1 || Hkv < 1 || Skv < 1 || Dl < 1 || Dr < 1) return TL_ERR_INVALID_VALUE;
+  if (!std::isfinite(scale)) return TL_ERR_INVALID_VALUE;
+  if (dtype != TL_DTYPE_F16 && dtype != TL_DTYPE_BF16) return TL_ERR_INVALID_VALUE;
+  if (Dl != mla::DL || Dr != mla::DR || H % Hkv != 0) return TL_ERR_UNSUPPORTED;
+  auto al = [](const void* ptr, uintptr_t a) { return (reinterpret_cast<uintptr_t>(ptr) % a) == 0; };
+  if (!al(q, 16) || !al(q_pe, 16) || !al(kv, 16) || !al(k_pe, 16) || !al(o, 16) || !al(ws, 256))
+    return TL_ERR_UNSUPPORTED;
+  if ((lse && !al(lse, 4)) || (seqlens && !al(seqlens, 4))) return TL_ERR_UNSUPPORTED;
+  if ((long long)B * H > 0x7fffffffLL || (long long)B * Skv * Hkv > 0x7fffffffLL)
+    return TL_ERR_UNSUPPORTED;
+  int dev, rc;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  const MlaPlan pl = plan_mla(B, H, Hkv, dev, di->sm_count);
+  if (ws_bytes < pl.bytes) return TL_ERR_INVALID_VALUE;
+  if ((long long)pl.NHG * pl.P > 0x7fffffffLL || B > 65535 || pl.NHG > 65535) return TL_ERR_UNSUPPORTED;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  mla::MlaParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  const cuuint64_t HH = (cuuint64_t)H, BB = (cuuint64_t)B, SS = (cuuint64_t)Skv, GG = (cuuint64_t)Hkv;
+  if (!encode_4d(enc, &prm.tm_q, q, dtype, {(cuuint64_t)mla::DL, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
+      !encode_4d(enc, &prm.tm_qpe, q_pe, dtype, {(cuuint64_t)mla::DR, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
+      !encode_4d(enc, &prm.tm_k, kv, dtype, {(cuuint64_t)mla::DL, GG, SS, BB}, {64, 1, mla::BLK, 1}) ||
+      !encode_4d(enc, &prm.tm_v, kv, dtype, {(cuuint64_t)mla::DL, GG, SS, BB}, {64, 1, mla::BLK / 2, 1}) ||
+      !encode_4d(enc, &prm.tm_kpe, k_pe, dtype, {(cuuint64_t)mla::DR, GG, SS, BB}, {64, 1, mla::BLK, 1}))
+    return TL_ERR_CUDA;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  prm.o = o;
+  prm.lse = lse;
+  prm.seqlens = seqlens;
+  prm.cum = reinterpret_cast<int*>(wsb);
+  prm.ws_lse = reinterpret_cast<float*>(wsb + pl.off_lse);
+  prm.ws_o = reinterpret_cast<float*>(wsb + pl.off_o);
+  prm.B = B;
+  prm.H = H;
+  prm.Hkv = Hkv;
+  prm.Skv = Skv;
+  prm.g = H / Hkv;
+  prm.T = pl.T;
+  prm.P = pl.P;
+  prm.CL = pl.CL;
+  prm.c_log2 = std::fabs(scale) * 1.4426950408889634f;
+  if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;  // scale = 0: see tl_attn_fwd
+  prm.neg = scale < 0.f ? 1 : 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rc = dtype == TL_DTYPE_BF16 ? launch_mla<true>(prm, dev, B, seqlens, Skv, st)
+                              : launch_mla<false>(prm, dev, B, seqlens, Skv, st);
+  if (rc == TL_OK) g_last_launches = 3;
   return rc;
 }
 

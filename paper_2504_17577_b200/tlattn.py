@@ -54,6 +54,10 @@ def load_library(path: str | None = None):
         lib.tl_attn_version.restype = I
         lib.tl_gemm.argtypes = [P, P, P, I, I, I, I, P]
         lib.tl_gemm.restype = I
+        lib.tl_mla_decode.argtypes = [P, P, P, P, P, P, P, I, I, I, I, I, I, F, I, P, U64, P]
+        lib.tl_mla_decode.restype = I
+        lib.tl_mla_decode_workspace_bytes.argtypes = [I, I, I]
+        lib.tl_mla_decode_workspace_bytes.restype = U64
         lib.tl_attn_last_launch_count.argtypes = []
         lib.tl_attn_last_launch_count.restype = I
         _lib = lib
@@ -170,6 +174,49 @@ def gemm(a, b, out=None, stream=None):
     c = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
     tl_gemm(a, b, c, M, N, K, dtype_code(a.dtype), stream)
     return c
+
+
+def tl_mla_decode(q, q_pe, kv, k_pe, o, lse, seqlens, B, H, Hkv, Skv, Dl, Dr, scale, dtype,
+                  ws, ws_bytes, stream=None):
+    """Direct mirror of the C entry point (Fig. 18 MLA decode)."""
+    _check(load_library().tl_mla_decode(_ptr(q), _ptr(q_pe), _ptr(kv), _ptr(k_pe), _ptr(o),
+                                        _ptr(lse), _ptr(seqlens), int(B), int(H), int(Hkv),
+                                        int(Skv), int(Dl), int(Dr), float(scale), int(dtype),
+                                        _ptr(ws), int(ws_bytes), _stream_handle(stream)))
+
+
+def tl_mla_decode_workspace_bytes(B, H, Hkv) -> int:
+    return int(load_library().tl_mla_decode_workspace_bytes(int(B), int(H), int(Hkv)))
+
+
+def mla_decode(q, q_pe, kv, k_pe, seqlens=None, scale=None, return_lse=True, out=None,
+               lse_out=None, workspace=None, stream=None):
+    """MLA decode on the GPU: q[B,H,Dl], q_pe[B,H,Dr], kv[B,Skv,Hkv,Dl], k_pe[B,Skv,Hkv,Dr],
+    optional int32 seqlens[B]. Returns o[B,H,Dl] (and lse[B,H]). ``workspace`` is a uint8
+    CUDA tensor of >= tl_mla_decode_workspace_bytes(B, H, Hkv) bytes (allocated if None)."""
+    if q.dim() != 3 or q_pe.dim() != 3 or kv.dim() != 4 or k_pe.dim() != 4:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "expected q[B,H,Dl], q_pe[B,H,Dr], "
+                          "kv[B,Skv,Hkv,Dl], k_pe[B,Skv,Hkv,Dr]")
+    B, H, Dl = q.shape
+    _, Skv, Hkv, _ = kv.shape
+    Dr = q_pe.shape[2]
+    for t in (q, q_pe, kv, k_pe):
+        if not (t.is_cuda and t.is_contiguous() and t.dtype == q.dtype):
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "inputs must be contiguous CUDA tensors of one dtype")
+    if seqlens is not None and (seqlens.dtype != torch.int32 or not seqlens.is_cuda):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "seqlens must be a CUDA int32 tensor")
+    scale = 1.0 / math.sqrt(Dl + Dr) if scale is None else float(scale)
+    o = out if out is not None else torch.empty((B, H, Dl), dtype=q.dtype, device=q.device)
+    lse = None
+    if return_lse:
+        lse = lse_out if lse_out is not None else torch.empty((B, H), dtype=torch.float32,
+                                                              device=q.device)
+    nbytes = tl_mla_decode_workspace_bytes(B, H, Hkv)
+    if workspace is None:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device)
+    tl_mla_decode(q, q_pe, kv, k_pe, o, lse, seqlens, B, H, Hkv, Skv, Dl, Dr, scale,
+                  dtype_code(q.dtype), workspace, workspace.numel(), stream)
+    return (o, lse) if return_lse else o
 
 
 class HostAttention:

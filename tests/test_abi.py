@@ -24,13 +24,14 @@ def lib():
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(tl_attn_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(tl_\w+)\s*\(", src)))
 
 
 def test_header_declares_the_entry_points():
     names = declared_functions()
     for n in ("tl_attn_fwd", "tl_attn_fwd_host", "tl_attn_host_workspace_bytes",
-              "tl_attn_strerror", "tl_attn_version", "tl_attn_last_launch_count"):
+              "tl_attn_strerror", "tl_attn_version", "tl_attn_last_launch_count", "tl_gemm",
+              "tl_mla_decode", "tl_mla_decode_workspace_bytes"):
         assert n in names
 
 
@@ -103,3 +104,34 @@ def test_python_binding_fails_loudly_without_library(tmp_path):
             tlattn.load_library(str(tmp_path / "missing.so"))
         finally:
             tlattn._lib = saved
+
+
+# ---------------------------------------------------------------- tl_mla_decode
+MLA_GOOD = dict(q=FAKE, q_pe=FAKE, kv=FAKE, k_pe=FAKE, o=FAKE, lse=FAKE, seqlens=None, B=2, H=128,
+                Hkv=1, Skv=1024, Dl=512, Dr=64, scale=0.04, dtype=1, ws=FAKE, ws_bytes=1 << 40)
+
+
+def mla_call(lib, **over):
+    a = dict(MLA_GOOD, **over)
+    return lib.tl_mla_decode(a["q"], a["q_pe"], a["kv"], a["k_pe"], a["o"], a["lse"], a["seqlens"],
+                             a["B"], a["H"], a["Hkv"], a["Skv"], a["Dl"], a["Dr"], a["scale"],
+                             a["dtype"], a["ws"], a["ws_bytes"], None)
+
+
+@pytest.mark.parametrize("over,code", [
+    (dict(q=None), 1), (dict(q_pe=None), 1), (dict(kv=None), 1), (dict(k_pe=None), 1),
+    (dict(o=None), 1), (dict(ws=None), 1), (dict(B=0), 1), (dict(H=0), 1), (dict(Hkv=0), 1),
+    (dict(Skv=0), 1), (dict(Dr=0), 1), (dict(scale=float("nan")), 1), (dict(dtype=2), 1),
+    (dict(Dl=256), 2), (dict(Dr=32), 2), (dict(H=6, Hkv=4), 2), (dict(kv=FAKE + 8), 2),
+    (dict(lse=FAKE + 1), 2), (dict(seqlens=FAKE + 2), 2), (dict(ws=FAKE + 16), 2),
+    (dict(B=1 << 16, Skv=1 << 16), 2),
+])
+def test_mla_invalid_arguments_rejected(lib, over, code):
+    assert mla_call(lib, **over) == code
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_mla_without_device(lib):
+    assert mla_call(lib) == 3  # arguments valid, no device -> TL_ERR_CUDA (no fallback)
+    assert tlattn.tl_mla_decode_workspace_bytes(2, 128, 1) == 0  # needs the device's SM count
+    assert tlattn.tl_mla_decode_workspace_bytes(0, 128, 1) == 0
