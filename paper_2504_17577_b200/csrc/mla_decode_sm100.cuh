@@ -16,14 +16,15 @@
 // are warp transposed-butterfly reductions plus a 4-warp smem step; l is kept as
 // per-thread partial sums and reduced once per segment.
 //
-//   warp 0     TMA producer: Qhat (8 x [32 heads x 64] + q_pe) once per segment, then
-//              Khat chunks [128 keys x 64 dims] (8 of KV + 1 of K_pe) and V units
-//              [64 keys x 128 dv] into ONE ring of 16 KB slots, in MMA consumption order
-//              (S(0), S(1), PV(0), S(2), PV(1), ...). V is re-read (from L2) for PV rather
-//              than kept resident: a 128-key block of Khat is 144 KB, so keeping it until
-//              its PV would leave no room to prefetch the next block.
-//   warp 1     MMA issuer (one thread): S(j+1) before PV(j), so the tensor core computes the
-//              next scores while the softmax of block j runs.
+//   warp 0     TMA producer: Qhat (8 x [32 heads x 64] + q_pe) once per segment, then per
+//              key block the K_pe chunk and four "pair" slots (KV dims [128m, 128m+128) as two
+//              [128 keys x 64] SWIZZLE_128B boxes). The pair slots are both the QK^T operand
+//              and, unchanged, the V^T operand of PV: each KV byte crosses L2 -> SM once per
+//              head tile. Five pair slots = one resident block + one prefetched pair.
+//              (Measured: re-reading V from L2 instead costs 1.85x the L2 -> SM bytes, and on
+//              B200 L2 -> SM traffic saturates near the HBM rate.)
+//   warp 1     MMA issuer (one thread): S(j+1) part A (K_pe, pair 0) -> PV(j) -> S(j+1) part B,
+//              so the tensor core computes the next scores while the softmax of block j runs.
 //   warps 4-7  softmax + epilogue.
 // Work split (split-KV, the FlashDecoding / FlashMLA scheme; Fig. 18 has one CTA per
 // (batch, head block), which leaves most of 148 SMs idle at decode batch sizes): the key
@@ -50,9 +51,10 @@ constexpr int DR = 64;              // rope dim, Fig. 18 `pe_dim`
 constexpr int BLK = 128;            // keys per block (tcgen05 M of S^T)
 constexpr int HC = 32;              // query heads per CTA (tcgen05 N)
 constexpr int NKCH = DL / 64 + 1;   // Khat chunks per block: 8 of KV + 1 of K_pe
-constexpr int NVU = 8;              // V units per block: 4 dv chunks x 2 key halves
-constexpr int SLOT = 16384;         // ring slot: [128 keys x 64] or [2 x 64 keys x 64]
-constexpr int NSLOT = 10;
+constexpr int NPAIRS_PER_BLK = DL / 128;  // 4 pair slots per block: KV dims [128m, 128m+128)
+constexpr int SLOT = 16384;         // one [128 keys x 64] 16-bit SWIZZLE_128B box
+constexpr int NPAIR = 5;            // pair slots (2 x SLOT): one block resident + one prefetched
+constexpr int NPE = 1;              // K_pe slots
 constexpr int QCH = HC * 128;       // one [32 heads x 64] SW128 chunk of Qhat (4 KB)
 constexpr int PBYTES = BLK * HC * 2;  // P^T [128 keys x 32 heads] 16-bit, SW64 (8 KB)
 constexpr int THREADS = 256;
@@ -61,20 +63,15 @@ constexpr uint32_t TM_S = 0;        // S^T buffers at columns 0, 32
 constexpr uint32_t TM_O = 64;       // O^T dv chunk m at columns 64 + 32 m
 constexpr float RESCALE_LOG2 = 8.0f;  // conditional rescale threshold (as the attention kernel)
 
-// Experiments only (WRONG results): 1 = no softmax arithmetic (P = raw S bits),
-// 3 = no V loads / PV MMAs (K stream + softmax alone).
-#ifndef TLATTN_MLA_EXP
-#define TLATTN_MLA_EXP 0
-#endif
-
-constexpr int OFF_RING = 0;
-constexpr int OFF_Q = OFF_RING + NSLOT * SLOT;
+constexpr int OFF_PAIR = 0;
+constexpr int OFF_PE = OFF_PAIR + NPAIR * 2 * SLOT;
+constexpr int OFF_Q = OFF_PE + NPE * SLOT;
 constexpr int OFF_P = OFF_Q + NKCH * QCH;
-constexpr int OFF_RED = OFF_P + 2 * PBYTES;        // float red[2][4][32] + redl[4][32]
+constexpr int OFF_RED = OFF_P + PBYTES;            // float red[2][4][32] + redl[4][32]
 constexpr int OFF_BAR = OFF_RED + 3 * 4 * 32 * 4;
-// ring_full[NSLOT], ring_empty[NSLOT], q_full, q_empty, s_full[2], s_free[2], p_full[2],
-// o_done[2], o_free
-constexpr int NUM_BARS = 2 * NSLOT + 11;
+// pair_full/empty[NPAIR], pe_full/empty[NPE], q_full, q_empty, s_full[2], s_free[2], p_full,
+// o_done, o_free
+constexpr int NUM_BARS = 2 * NPAIR + 2 * NPE + 9;
 constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
 constexpr int SMEM_USED = OFF_TMEMPTR + 16;
 constexpr int SMEM_BYTES = SMEM_USED + 1024;
@@ -84,7 +81,6 @@ struct MlaParams {
   CUtensorMap tm_q;    // q   [B][H][DL]       as (DL, H, 1, B),   box (64, 32, 1, 1)
   CUtensorMap tm_qpe;  // q_pe[B][H][DR]       as (DR, H, 1, B),   box (64, 32, 1, 1)
   CUtensorMap tm_k;    // kv  [B][Skv][Hkv][DL] as (DL, Hkv, Skv, B), box (64, 1, 128, 1)
-  CUtensorMap tm_v;    // kv, box (64, 1, 64, 1)
   CUtensorMap tm_kpe;  // k_pe[B][Skv][Hkv][DR], box (64, 1, 128, 1)
   void* o;             // [B][H][DL]
   float* lse;          // [B][H] natural log, or nullptr
@@ -178,21 +174,25 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw_u32);
-  const uint32_t sRing = base + OFF_RING;
+  const uint32_t sPair = base + OFF_PAIR;
+  const uint32_t sPe = base + OFF_PE;
   const uint32_t sQ = base + OFF_Q;
   const uint32_t sP = base + OFF_P;
   float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][32]
   float* redl = red + 2 * 4 * 32;                          // [4][32]
   const uint32_t bar0 = base + OFF_BAR;
-  auto bar_full = [&](int s) { return bar0 + 8u * s; };
-  auto bar_empty = [&](int s) { return bar0 + 8u * (NSLOT + s); };
-  const uint32_t bar_q_full = bar0 + 8u * (2 * NSLOT);
-  const uint32_t bar_q_empty = bar_q_full + 8u;
-  auto bar_s_full = [&](int i) { return bar0 + 8u * (2 * NSLOT + 2 + i); };
-  auto bar_s_free = [&](int i) { return bar0 + 8u * (2 * NSLOT + 4 + i); };
-  auto bar_p_full = [&](int i) { return bar0 + 8u * (2 * NSLOT + 6 + i); };
-  auto bar_o_done = [&](int i) { return bar0 + 8u * (2 * NSLOT + 8 + i); };
-  const uint32_t bar_o_free = bar0 + 8u * (2 * NSLOT + 10);
+  auto bar_pair_full = [&](int s) { return bar0 + 8u * s; };
+  auto bar_pair_empty = [&](int s) { return bar0 + 8u * (NPAIR + s); };
+  auto bar_pe_full = [&](int s) { return bar0 + 8u * (2 * NPAIR + s); };
+  auto bar_pe_empty = [&](int s) { return bar0 + 8u * (2 * NPAIR + NPE + s); };
+  const uint32_t bar_x = bar0 + 8u * (2 * NPAIR + 2 * NPE);
+  const uint32_t bar_q_full = bar_x;
+  const uint32_t bar_q_empty = bar_x + 8u;
+  auto bar_s_full = [&](int i) { return bar_x + 8u * (2 + i); };
+  auto bar_s_free = [&](int i) { return bar_x + 8u * (4 + i); };
+  const uint32_t bar_p_full = bar_x + 8u * 6;
+  const uint32_t bar_o_done = bar_x + 8u * 7;
+  const uint32_t bar_o_free = bar_x + 8u * 8;
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -212,20 +212,23 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     prefetch_tmap(&p.tm_q);
     prefetch_tmap(&p.tm_qpe);
     prefetch_tmap(&p.tm_k);
-    prefetch_tmap(&p.tm_v);
     prefetch_tmap(&p.tm_kpe);
-    for (int s = 0; s < NSLOT; ++s) {
-      mbar_init(bar_full(s), 1);
-      mbar_init(bar_empty(s), p.CL);  // released by the MMA of every CTA of the cluster
+    for (int s = 0; s < NPAIR; ++s) {
+      mbar_init(bar_pair_full(s), 1);
+      mbar_init(bar_pair_empty(s), p.CL);  // released by the PV MMAs of every CTA of the cluster
+    }
+    for (int s = 0; s < NPE; ++s) {
+      mbar_init(bar_pe_full(s), 1);
+      mbar_init(bar_pe_empty(s), p.CL);
     }
     mbar_init(bar_q_full, 1);
     mbar_init(bar_q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_s_full(i), 1);
       mbar_init(bar_s_free(i), 4);
-      mbar_init(bar_p_full(i), 4);
-      mbar_init(bar_o_done(i), 1);
     }
+    mbar_init(bar_p_full, 4);
+    mbar_init(bar_o_done, 1);
     mbar_init(bar_o_free, 4);
     fence_mbar_init();
   }
@@ -238,28 +241,19 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
 
   if (warp == 0) {
     // ================================ TMA producer ================================
-    // Ring slots are filled by multicast: unit `it` is loaded by CTA (it % CL) into the same
-    // slot of every CTA of the cluster; a slot is refilled only after all CL MMAs released it.
+    // Block j of a segment = K_pe chunk (pe ring) + 4 pair slots, pair m = KV dims
+    // [128m, 128m+128) as two [128 keys x 64] SWIZZLE_128B boxes. The pair slots stay
+    // resident from S(j) to PV(j) (they are both the QK^T operand and V). With CL > 1, unit
+    // number u (pairs and pe counted separately) is loaded by CTA (u % CL) and multicast.
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
-      const uint64_t pol_k = policy_evict_last();   // re-read as V and by the other head tiles
-      const uint64_t pol_v = policy_evict_last();
-      uint32_t it = 0;
+      const uint64_t pol_kv = policy_evict_first();  // streamed once (per head tile)
+      uint32_t pit = 0, eit = 0;
       int nseg = 0;
       SegIter si(p, part);
       Seg sg;
-      bool mine = true;  // this CTA issues the current unit's load
-      auto acquire = [&](uint32_t& slot_addr) -> uint32_t {
-        const int slot = it % NSLOT;
-        if (it >= (uint32_t)NSLOT) mbar_wait(bar_empty(slot), ((it / NSLOT) - 1) & 1);
-        mbar_arrive_expect_tx(bar_full(slot), SLOT);
-        slot_addr = sRing + slot * SLOT;
-        mine = (it % p.CL) == rank;
-        ++it;
-        return bar_full(slot);
-      };
-      auto load = [&](uint32_t dst, const CUtensorMap* m, uint32_t fb, int c0, int c1, int c2, int c3,
-                      uint64_t pol) {
+      auto load = [&](bool mine, uint32_t dst, const CUtensorMap* m, uint32_t fb, int c0, int c1,
+                      int c2, int c3, uint64_t pol) {
         if (!mine) return;
         if (p.CL > 1) tma_load_4d_mc(dst, m, fb, c0, c1, c2, c3, mc_mask, pol);
         else tma_load_4d(dst, m, fb, c0, c1, c2, c3, pol);
@@ -272,27 +266,27 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
           tma_load_4d(sQ + c * QCH, &p.tm_q, bar_q_full, c * 64, h0, 0, sg.b, pol_q);
         tma_load_4d(sQ + (DL / 64) * QCH, &p.tm_qpe, bar_q_full, 0, h0, 0, sg.b, pol_q);
 #pragma unroll 1
-        for (int jj = 0; jj <= sg.n; ++jj) {
-          if (jj < sg.n) {  // Khat(j): 8 KV chunks + K_pe
-            const int key0 = (sg.k0 + jj) * BLK;
-#pragma unroll 1
-            for (int c = 0; c < NKCH; ++c) {
-              uint32_t dst;
-              const uint32_t fb = acquire(dst);
-              if (c < DL / 64) load(dst, &p.tm_k, fb, c * 64, kvh, key0, sg.b, pol_k);
-              else load(dst, &p.tm_kpe, fb, 0, kvh, key0, sg.b, pol_k);
-            }
+        for (int jj = 0; jj < sg.n; ++jj) {
+          const int key0 = (sg.k0 + jj) * BLK;
+          {  // K_pe chunk
+            const int s = eit % NPE;
+            if (eit >= (uint32_t)NPE) mbar_wait(bar_pe_empty(s), ((eit / NPE) - 1) & 1);
+            mbar_arrive_expect_tx(bar_pe_full(s), SLOT);
+            load((eit % p.CL) == rank, sPe + s * SLOT, &p.tm_kpe, bar_pe_full(s), 0, kvh, key0,
+                 sg.b, pol_kv);
+            ++eit;
           }
-          if (jj >= 1 && TLATTN_MLA_EXP != 3) {  // V(j-1): unit u = dv chunk (u>>1), key half (u&1)
-            const int key0 = (sg.k0 + jj - 1) * BLK;
 #pragma unroll 1
-            for (int u = 0; u < NVU; ++u) {
-              uint32_t dst;
-              const uint32_t fb = acquire(dst);
-              const int m = u >> 1, hf = u & 1;
-              load(dst, &p.tm_v, fb, (2 * m) * 64, kvh, key0 + hf * 64, sg.b, pol_v);
-              load(dst + SLOT / 2, &p.tm_v, fb, (2 * m + 1) * 64, kvh, key0 + hf * 64, sg.b, pol_v);
-            }
+          for (int m = 0; m < NPAIRS_PER_BLK; ++m) {
+            const int s = pit % NPAIR;
+            if (pit >= (uint32_t)NPAIR) mbar_wait(bar_pair_empty(s), ((pit / NPAIR) - 1) & 1);
+            mbar_arrive_expect_tx(bar_pair_full(s), 2 * SLOT);
+            const bool mine = (pit % p.CL) == rank;
+            load(mine, sPair + s * 2 * SLOT, &p.tm_k, bar_pair_full(s), (2 * m) * 64, kvh, key0, sg.b,
+                 pol_kv);
+            load(mine, sPair + s * 2 * SLOT + SLOT, &p.tm_k, bar_pair_full(s), (2 * m + 1) * 64, kvh,
+                 key0, sg.b, pol_kv);
+            ++pit;
           }
         }
         ++nseg;
@@ -301,77 +295,98 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     __syncwarp();
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
+    // Per block: S(j+1) part A (K_pe + pair 0, which fit in the free slots) -> PV(j) (frees the
+    // pair slots of block j) -> S(j+1) part B (pairs 1-3). The tensor core computes the next
+    // scores while softmax(j) runs.
     if (lane == 0) {
       constexpr uint32_t FMT = BF16 ? 1u : 0u;
       // S^T = Khat Qhat^T: A = Khat (K-major), B = Qhat (K-major), M=128 keys, N=HC heads
       const uint32_t IDESC_S = make_idesc_f16(FMT, BLK, HC, 0, 0, 0) | ((p.neg ? 1u : 0u) << 14);
       // O^T += V^T P^T: A = V^T (MN-major: dv contiguous), B = P^T (MN-major: heads
-      // contiguous), M=128 dv, N=HC heads
+      // contiguous), M=128 dv, N=HC heads, K=128 keys
       constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, 128, HC, 1, 1, 0);
-      uint32_t it = 0;
-      uint32_t gb = 0;  // global block counter (S / P buffer phases)
+      uint32_t pit = 0, eit = 0;  // pair / pe ring positions (same sequence as the producer)
+      uint32_t gb = 0;            // global block counter
       int nseg = 0;
       SegIter si(p, part);
       Seg sg;
-      auto wait_slot = [&]() -> uint32_t {
-        const int slot = it % NSLOT;
-        mbar_wait(bar_full(slot), (it / NSLOT) & 1);
+      // S^T(gs) += Khat chunk(s) . Qhat chunk(c)
+      auto s_chunk = [&](uint32_t sb, uint32_t a0, int c, bool first) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_f16_ss(tmem_base + TM_S + sb * HC, make_sdesc(a0 + kk * 32, 16, 1024, 2),
+                     make_sdesc(sQ + c * QCH + kk * 32, 16, 1024, 2), IDESC_S,
+                     (first && kk == 0) ? 0u : 1u);
+      };
+      auto s_pe = [&](uint32_t sb) {  // K_pe chunk (first MMAs of S(gs))
+        const int s = eit % NPE;
+        mbar_wait(bar_pe_full(s), (eit / NPE) & 1);
         tc_fence_after();
-        return slot;
+        s_chunk(sb, sPe + s * SLOT, DL / 64, true);
+        if (p.CL > 1) mma_commit_mc(bar_pe_empty(s), mc_mask);
+        else mma_commit(bar_pe_empty(s));
+        ++eit;
+      };
+      auto s_pair = [&](uint32_t sb, uint32_t pos, int m) {
+        const int s = pos % NPAIR;
+        mbar_wait(bar_pair_full(s), (pos / NPAIR) & 1);
+        tc_fence_after();
+        s_chunk(sb, sPair + s * 2 * SLOT, 2 * m, false);
+        s_chunk(sb, sPair + s * 2 * SLOT + SLOT, 2 * m + 1, false);
+      };
+      auto s_begin = [&](uint32_t gs) {
+        if (gs >= 2) mbar_wait(bar_s_free(gs & 1), ((gs - 2) >> 1) & 1);
+        tc_fence_after();
       };
       while (si.next(p, sg)) {
         mbar_wait(bar_q_full, nseg & 1);
         tc_fence_after();
+        const uint32_t pit0 = pit;  // pair position of block 0 of this segment, pair 0
+        // S(0), whole
+        s_begin(gb);
+        s_pe(gb & 1);
 #pragma unroll 1
-        for (int jj = 0; jj <= sg.n; ++jj) {
-          if (jj < sg.n) {  // S(gb + jj)
-            const uint32_t gs = gb + jj;
-            const uint32_t sb = gs & 1;
-            if (gs >= 2) mbar_wait(bar_s_free(sb), ((gs - 2) >> 1) & 1);
-            tc_fence_after();
+        for (int m = 0; m < NPAIRS_PER_BLK; ++m) s_pair(gb & 1, pit0 + m, m);
+        mma_commit(bar_s_full(gb & 1));
+        if (sg.n == 1) mma_commit(bar_q_empty);
 #pragma unroll 1
-            for (int c = 0; c < NKCH; ++c) {
-              const int slot = wait_slot();
-              const uint32_t a0 = sRing + slot * SLOT;
-              const uint32_t b0 = sQ + c * QCH;
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_f16_ss(tmem_base + TM_S + sb * HC, make_sdesc(a0 + kk * 32, 16, 1024, 2),
-                           make_sdesc(b0 + kk * 32, 16, 1024, 2), IDESC_S, (c | kk) ? 1u : 0u);
-              if (p.CL > 1) mma_commit_mc(bar_empty(slot), mc_mask);
-              else mma_commit(bar_empty(slot));
-              ++it;
-            }
-            mma_commit(bar_s_full(sb));
-            if (jj == sg.n - 1) mma_commit(bar_q_empty);
+        for (int jj = 0; jj < sg.n; ++jj) {
+          const uint32_t g = gb + jj;
+          const uint32_t pos = pit0 + NPAIRS_PER_BLK * jj;  // pair 0 of block jj
+          const bool more = jj + 1 < sg.n;
+          if (more) {  // S(j+1) part A
+            s_begin(g + 1);
+            s_pe((g + 1) & 1);
+            s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK, 0);
           }
-          if (jj >= 1) {  // PV(gb + jj - 1)
-            const uint32_t gp = gb + jj - 1;
-            const uint32_t pb = gp & 1;
-            if (jj == 1 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
-            mbar_wait(bar_p_full(pb), (gp >> 1) & 1);
-            tc_fence_after();
+          // PV(j)
+          if (jj == 0 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
+          mbar_wait(bar_p_full, g & 1);
+          tc_fence_after();
 #pragma unroll 1
-            for (int u = 0; u < (TLATTN_MLA_EXP == 3 ? 0 : NVU); ++u) {
-              const int m = u >> 1, hf = u & 1;
-              const int slot = wait_slot();
-              const uint32_t a0 = sRing + slot * SLOT;
-              const uint32_t b0 = sP + pb * PBYTES + hf * (64 * 64);
+          for (int m = 0; m < NPAIRS_PER_BLK; ++m) {
+            const int s = (pos + m) % NPAIR;
+            const uint32_t a0 = sPair + s * 2 * SLOT;
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                // A: V^T MN-major SW128, 16 keys = 16 rows of 128 B; LBO = 8 KB to the next
-                // 64-wide dv atom. B: P^T MN-major SW64, 16 keys = 16 rows of 64 B.
-                mma_f16_ss(tmem_base + TM_O + m * HC, make_sdesc(a0 + kk * 2048, SLOT / 2, 1024, 2),
-                           make_sdesc(b0 + kk * 1024, 4096, 512, 4), IDESC_PV,
-                           (jj > 1 || hf > 0 || kk > 0) ? 1u : 0u);
-              }
-              if (p.CL > 1) mma_commit_mc(bar_empty(slot), mc_mask);
-              else mma_commit(bar_empty(slot));
-              ++it;
+            for (int kk = 0; kk < BLK / 16; ++kk) {
+              // A: V^T MN-major SW128, 16 keys = 16 rows of 128 B; LBO = 16 KB to the second
+              // 64-wide dv atom of the pair. B: P^T MN-major SW64, 16 keys = 16 rows of 64 B.
+              mma_f16_ss(tmem_base + TM_O + m * HC, make_sdesc(a0 + kk * 2048, SLOT, 1024, 2),
+                         make_sdesc(sP + kk * 1024, 4096, 512, 4), IDESC_PV,
+                         (jj > 0 || kk > 0) ? 1u : 0u);
             }
-            mma_commit(bar_o_done(pb));
+            if (p.CL > 1) mma_commit_mc(bar_pair_empty(s), mc_mask);
+            else mma_commit(bar_pair_empty(s));
+          }
+          mma_commit(bar_o_done);
+          if (more) {  // S(j+1) part B
+#pragma unroll 1
+            for (int m = 1; m < NPAIRS_PER_BLK; ++m) s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK + m, m);
+            mma_commit(bar_s_full((g + 1) & 1));
+            if (jj + 2 == sg.n) mma_commit(bar_q_empty);
           }
         }
+        pit += NPAIRS_PER_BLK * sg.n;
         gb += sg.n;
         ++nseg;
       }
@@ -405,14 +420,6 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s_free(sb));
-        uint32_t pk[HC / 2];
-        bool resc = false;
-        float m_new = m;
-        float alpha = 1.f;
-        if constexpr (TLATTN_MLA_EXP == 1) {
-#pragma unroll
-          for (int h = 0; h < HC / 2; ++h) pk[h] = __float_as_uint(s[2 * h]);
-        } else {
         // tail mask: keys >= len of this batch do not take part (TMA zero-fills beyond Skv)
         if ((sg.k0 + jj) * BLK + row >= sg.len) {
 #pragma unroll
@@ -438,11 +445,12 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         named_bar_sync(1, 128);
         const float mx = fmaxf(fmaxf(rb[lane], rb[32 + lane]), fmaxf(rb[64 + lane], rb[96 + lane]));
         const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
-        m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
+        const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        alpha = ex2(m - m_use);  // scores_scale; 0 on the first block
+        const float alpha = ex2(m - m_use);  // scores_scale; 0 on the first block
         // p = exp2(s c - m_head), l partial sums from the unrounded p (R8)
-        resc = __any_sync(FULL, alpha != 1.f);
+        uint32_t pk[HC / 2];
+        const bool resc = __any_sync(FULL, alpha != 1.f);
 #pragma unroll
         for (int h = 0; h < HC; h += 2) {
           const float m0 = __shfl_sync(FULL, m_use, h);
@@ -457,12 +465,10 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
           lpart[h + 1] += p1;
           pk[h / 2] = pack2<BF16>(p0, p1);  // P rounded RN to the dtype (S_shared)
         }
-        }
-        // P^T buffer sb is free once PV(gs-2) completed
-        if (gs >= 2) mbar_wait(bar_o_done(sb), ((gs - 2) >> 1) & 1);
+        // the P^T buffer and O^T are free once PV(gs-1) completed
+        if (gs >= 1) mbar_wait(bar_o_done, (gs - 1) & 1);
         if (resc && jj > 0) {
-          // acc_o *= scores_scale: O^T columns are heads; needs PV(gs-1) done
-          mbar_wait(bar_o_done(sb ^ 1), ((gs - 1) >> 1) & 1);
+          // acc_o *= scores_scale: O^T columns are heads
           tc_fence_after();
           float al[HC];
 #pragma unroll
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         }
         // P^T row (this key, 32 heads = 64 B) -> smem, MN-major SWIZZLE_64B:
         // 16-B unit u of row r lands at u ^ ((r >> 1) & 3)
-        const uint32_t prow = sP + sb * PBYTES + row * 64;
+        const uint32_t prow = sP + row * 64;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           st_shared_v4(prow + ((u ^ ((row >> 1) & 3)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
@@ -488,12 +494,12 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_p_full(sb));
+        if (lane == 0) mbar_arrive(bar_p_full);
         m = m_new;
       }
       // ---- epilogue: l = sum of the partial sums, O = O^T / l, LSE
       const uint32_t glast = gb + sg.n - 1;
-      mbar_wait(bar_o_done(glast & 1), (glast >> 1) & 1);
+      mbar_wait(bar_o_done, glast & 1);
       tc_fence_after();
       {
         float v[HC];

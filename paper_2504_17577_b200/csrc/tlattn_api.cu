@@ -552,7 +552,6 @@ extern "C" int tl_mla_decode(const void* q, const void* q_pe, const void* kv, co
   if (!encode_4d(enc, &prm.tm_q, q, dtype, {(cuuint64_t)mla::DL, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
       !encode_4d(enc, &prm.tm_qpe, q_pe, dtype, {(cuuint64_t)mla::DR, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
       !encode_4d(enc, &prm.tm_k, kv, dtype, {(cuuint64_t)mla::DL, GG, SS, BB}, {64, 1, mla::BLK, 1}) ||
-      !encode_4d(enc, &prm.tm_v, kv, dtype, {(cuuint64_t)mla::DL, GG, SS, BB}, {64, 1, mla::BLK / 2, 1}) ||
       !encode_4d(enc, &prm.tm_kpe, k_pe, dtype, {(cuuint64_t)mla::DR, GG, SS, BB}, {64, 1, mla::BLK, 1}))
     return TL_ERR_CUDA;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
