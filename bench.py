@@ -345,6 +345,9 @@ def run_ours(args, world, rank, local):
             extra[name] = bench_one(CONFIGS[name], pk, steps=max(5, min(args.steps, 20)))
         for gname in ("M5", "M2"):  # the paper's GEMM on Table 2 shapes
             extra["gemm_" + gname] = bench_gemm(gname, pk)
+        from paper_2504_17577_b200.configs import MLA_CONFIGS
+        for mc in MLA_CONFIGS:  # MLA decode (Fig. 18)
+            extra["mla_" + mc.name] = bench_mla(mc, pk, steps=max(5, min(args.steps, 20)))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -412,6 +415,46 @@ def bench_one(cfg, pk, steps=20, warmup=3):
     if small:
         res["note"] = "L2 flushed between launches (256 MB write)"
     del q, k, v, o, lse
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_mla(cfg, pk, steps=20, warmup=3):
+    """tl_mla_decode on an MLA config (inputs > L2). Bound: HBM (the latent cache is read
+    once; 235 FLOP/B at 128 heads is just below the bf16 ridge, 30 FLOP/B at 16 heads)."""
+    from paper_2504_17577_b200 import (mla_decode, tl_attn_last_launch_count,
+                                       tl_mla_decode_workspace_bytes)
+    from paper_2504_17577_b200.inputs import gen_mla
+    q, qp, kv, kp = gen_mla(cfg.B, cfg.H, cfg.Hkv, cfg.Skv, cfg.Dl, cfg.Dr, cfg.dtype, cfg.seed,
+                            "cuda")
+    sl = cfg.seqlens()
+    sld = None if sl is None else torch.as_tensor(sl, device="cuda")
+    ws = torch.empty(tl_mla_decode_workspace_bytes(cfg.B, cfg.H, cfg.Hkv), dtype=torch.uint8,
+                     device="cuda")
+    o = torch.empty((cfg.B, cfg.H, cfg.Dl), dtype=cfg.dtype, device="cuda")
+    lse = torch.empty((cfg.B, cfg.H), dtype=torch.float32, device="cuda")
+
+    def call():
+        mla_decode(q, qp, kv, kp, seqlens=sld, out=o, lse_out=lse, workspace=ws)
+
+    for _ in range(warmup):
+        call()
+    st = torch.cuda.current_stream()
+    evs = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        call()
+        b.record(st)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    gbs = cfg.hbm_bytes() / (ms * 1e-3) / 1e9
+    tf = cfg.flops() / (ms * 1e-3) / 1e12
+    res = {"us": ms * 1e3, "hbm_gbs": gbs, "frac_of_hbm": gbs / pk["hbm"], "tflops": tf,
+           "frac_of_peak": tf / pk["burst"], "launches_per_call": tl_attn_last_launch_count(),
+           "bound": "hbm", **cfg.as_dict()}
+    del q, qp, kv, kp, o, lse, ws
     torch.cuda.empty_cache()
     return res
 
