@@ -79,6 +79,16 @@ CONFIGS = {
                      "north_star target: D=128 non-causal S=8192 (C3 inputs, causal off)"),
 }
 
+# The paper's own FlashAttention shapes (Table 3: batch 1, 32 heads (R13),
+# head dim 128, S in {512, 1024, 4096}); context set, SURVEY §8(d). dtype bf16 (R14).
+PAPER_T3 = {
+    "FA0": AttnConfig("FA0", 1, 32, 32, 512, 512, 128, torch.bfloat16, True, 1010, "Table 3 FA0"),
+    "FA1": AttnConfig("FA1", 1, 32, 32, 512, 512, 128, torch.bfloat16, False, 1011, "Table 3 FA1"),
+    "FA2": AttnConfig("FA2", 1, 32, 32, 1024, 1024, 128, torch.bfloat16, True, 1012, "Table 3 FA2"),
+    "FA3": AttnConfig("FA3", 1, 32, 32, 1024, 1024, 128, torch.bfloat16, False, 1013, "Table 3 FA3"),
+    "FA4": AttnConfig("FA4", 1, 32, 32, 4096, 4096, 128, torch.bfloat16, True, 1014, "Table 3 FA4"),
+}
+
 
 # ------------------------------------------------------------------ MLA decode
 @dataclass(frozen=True)

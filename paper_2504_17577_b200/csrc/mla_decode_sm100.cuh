@@ -49,37 +49,51 @@ namespace mla {
 constexpr int DL = 512;             // latent (kv_lora) dim, Fig. 18 `dim`
 constexpr int DR = 64;              // rope dim, Fig. 18 `pe_dim`
 constexpr int BLK = 128;            // keys per block (tcgen05 M of S^T)
-constexpr int HC = 32;              // query heads per CTA (tcgen05 N)
 constexpr int NKCH = DL / 64 + 1;   // Khat chunks per block: 8 of KV + 1 of K_pe
 constexpr int NPAIRS_PER_BLK = DL / 128;  // 4 pair slots per block: KV dims [128m, 128m+128)
 constexpr int SLOT = 16384;         // one [128 keys x 64] 16-bit SWIZZLE_128B box
-constexpr int NPAIR = 5;            // pair slots (2 x SLOT): one block resident + one prefetched
-constexpr int NPE = 1;              // K_pe slots
-constexpr int QCH = HC * 128;       // one [32 heads x 64] SW128 chunk of Qhat (4 KB)
-constexpr int PBYTES = BLK * HC * 2;  // P^T [128 keys x 32 heads] 16-bit, SW64 (8 KB)
 constexpr int THREADS = 256;
-constexpr uint32_t TMEM_COLS = 256;
-constexpr uint32_t TM_S = 0;        // S^T buffers at columns 0, 32
-constexpr uint32_t TM_O = 64;       // O^T dv chunk m at columns 64 + 32 m
 constexpr float RESCALE_LOG2 = 8.0f;  // conditional rescale threshold (as the attention kernel)
+constexpr int HC_MAX = 64;
 
-constexpr int OFF_PAIR = 0;
-constexpr int OFF_PE = OFF_PAIR + NPAIR * 2 * SLOT;
-constexpr int OFF_Q = OFF_PE + NPE * SLOT;
-constexpr int OFF_P = OFF_Q + NKCH * QCH;
-constexpr int OFF_RED = OFF_P + PBYTES;            // float red[2][4][32] + redl[4][32]
-constexpr int OFF_BAR = OFF_RED + 3 * 4 * 32 * 4;
-// pair_full/empty[NPAIR], pe_full/empty[NPE], q_full, q_empty, s_full[2], s_free[2], p_full,
-// o_done, o_free
-constexpr int NUM_BARS = 2 * NPAIR + 2 * NPE + 9;
-constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
-constexpr int SMEM_USED = OFF_TMEMPTR + 16;
-constexpr int SMEM_BYTES = SMEM_USED + 1024;
-static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+// Per head-tile width HC (query heads per CTA = tcgen05 N of both MMAs):
+//  HC = 32: SMEM = 5 pair slots (one block resident + one pair prefetched) + K_pe slot +
+//           Qhat 36 KB + P^T 8 KB (64-B rows, SWIZZLE_64B);
+//  HC = 64: SMEM = 4 pair slots + K_pe slot + Qhat 72 KB; P^T (128-B rows, SWIZZLE_128B,
+//           16 KB) shares the K_pe slot (K_pe(j) is consumed by S(j) before softmax(j)
+//           writes P^T(j); K_pe(j+1) is loaded after PV(j) read it), so block j+1 is
+//           loaded while PV(j) frees the pair slots (no prefetch).
+template <int HC>
+struct Cfg {
+  static_assert(HC == 32 || HC == 64, "head tile");
+  static constexpr int R = HC / 32;                  // heads per lane after the butterfly
+  static constexpr bool PREFETCH = HC == 32;
+  static constexpr int NPAIR = PREFETCH ? 5 : 4;
+  static constexpr int QCH = HC * 128;               // one [HC heads x 64] SW128 chunk of Qhat
+  static constexpr int PBYTES = BLK * HC * 2;        // P^T [128 keys x HC heads]
+  static constexpr uint32_t P_LAYOUT = HC == 32 ? 4u : 2u;  // SWIZZLE_64B / SWIZZLE_128B
+  static constexpr uint32_t P_ROW = HC * 2;          // bytes per key row of P^T
+  static constexpr uint32_t TM_S = 0;                // S^T buffers at columns 0, HC
+  static constexpr uint32_t TM_O = 2 * HC;           // O^T dv chunk m at 2 HC + HC m
+  static constexpr uint32_t TMEM_COLS = HC == 32 ? 256 : 512;
+  static constexpr int OFF_PAIR = 0;
+  static constexpr int OFF_PE = OFF_PAIR + NPAIR * 2 * SLOT;
+  static constexpr int OFF_Q = OFF_PE + SLOT;
+  static constexpr int OFF_P = PREFETCH ? OFF_Q + NKCH * QCH : OFF_PE;
+  static constexpr int OFF_RED = OFF_Q + NKCH * QCH + (PREFETCH ? PBYTES : 0);
+  static constexpr int OFF_BAR = OFF_RED + 3 * 4 * HC * 4;  // red[2][4][HC] + redl[4][HC]
+  // pair_full/empty[NPAIR], pe_full, pe_empty, q_full, q_empty, s_full[2], s_free[2], p_full,
+  // o_done, o_free
+  static constexpr int NUM_BARS = 2 * NPAIR + 2 + 9;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16 + 1024;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+  static_assert(PREFETCH || PBYTES <= SLOT, "P^T must fit the K_pe slot");
+};
 
 struct MlaParams {
-  CUtensorMap tm_q;    // q   [B][H][DL]       as (DL, H, 1, B),   box (64, 32, 1, 1)
-  CUtensorMap tm_qpe;  // q_pe[B][H][DR]       as (DR, H, 1, B),   box (64, 32, 1, 1)
+  CUtensorMap tm_q;    // q   [B][H][DL]       as (DL, H, 1, B),   box (64, HC, 1, 1)
+  CUtensorMap tm_qpe;  // q_pe[B][H][DR]       as (DR, H, 1, B),   box (64, HC, 1, 1)
   CUtensorMap tm_k;    // kv  [B][Skv][Hkv][DL] as (DL, Hkv, Skv, B), box (64, 1, 128, 1)
   CUtensorMap tm_kpe;  // k_pe[B][Skv][Hkv][DR], box (64, 1, 128, 1)
   void* o;             // [B][H][DL]
@@ -88,6 +102,7 @@ struct MlaParams {
   int* cum;            // workspace: [B+1] prefix sums of key blocks per batch
   float* ws_o;         // workspace: [NHG][P][2][HC][DL] partial O (normalised)
   float* ws_lse;       // workspace: [NHG][P][2][HC] partial lse (log2 units)
+  int HC;              // query heads per CTA (32 or 64)
   int B, H, Hkv, Skv;
   int g;               // H / Hkv (query heads per kv head)
   int T;               // head tiles per kv head = ceil(g / HC)
@@ -168,24 +183,69 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-template <bool BF16>
+// Column reduction over the 32 lanes of a warp, "transposed butterfly": in[HC] per lane; on
+// exit v[i] (i < HC/32) holds op over the warp of column lane*(HC/32) + i. Each round halves
+// the columns a lane keeps (one shuffle per kept column), 31*(HC/32) shuffles in all.
+template <int HC, bool MAX>
+__device__ __forceinline__ void col_reduce(const float (&in)[HC], float (&v)[HC / 2], int lane) {
+  {  // first round (lane distance 16) straight from `in`
+    const bool up = (lane & 16) != 0;
+#pragma unroll
+    for (int i = 0; i < HC / 2; ++i) {
+      const float send = up ? in[i] : in[i + HC / 2];
+      const float keep = up ? in[i + HC / 2] : in[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, 16);
+      v[i] = MAX ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  int n = HC / 2;
+#pragma unroll
+  for (int d = 8; d >= 1; d >>= 1) {
+    const int half = n / 2;
+    const bool up = (lane & d) != 0;
+#pragma unroll
+    for (int i = 0; i < HC / 4; ++i) {
+      if (i < half) {
+        const float send = up ? v[i] : v[i + half];
+        const float keep = up ? v[i + half] : v[i];
+        const float got = __shfl_xor_sync(0xffffffffu, send, d);
+        v[i] = MAX ? fmaxf(keep, got) : keep + got;
+      }
+    }
+    n = half;
+  }
+}
+
+// value of per-head quantity x (lane l holds heads l*R .. l*R+R-1 in x[0..R-1]) for head h
+template <int R>
+__device__ __forceinline__ float head_val(const float (&x)[R], int h) {
+  float r = x[0];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if ((h % R) == i) r = __shfl_sync(0xffffffffu, x[i], h / R);
+  return r;
+}
+
+template <int HC, bool BF16>
 __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_constant__ MlaParams p) {
+  using C = Cfg<HC>;
+  constexpr int R = C::R;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw_u32);
-  const uint32_t sPair = base + OFF_PAIR;
-  const uint32_t sPe = base + OFF_PE;
-  const uint32_t sQ = base + OFF_Q;
-  const uint32_t sP = base + OFF_P;
-  float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2][4][32]
-  float* redl = red + 2 * 4 * 32;                          // [4][32]
-  const uint32_t bar0 = base + OFF_BAR;
+  const uint32_t sPair = base + C::OFF_PAIR;
+  const uint32_t sPe = base + C::OFF_PE;
+  const uint32_t sQ = base + C::OFF_Q;
+  const uint32_t sP = base + C::OFF_P;
+  float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2][4][HC]
+  float* redl = red + 2 * 4 * HC;                             // [4][HC]
+  const uint32_t bar0 = base + C::OFF_BAR;
   auto bar_pair_full = [&](int s) { return bar0 + 8u * s; };
-  auto bar_pair_empty = [&](int s) { return bar0 + 8u * (NPAIR + s); };
-  auto bar_pe_full = [&](int s) { return bar0 + 8u * (2 * NPAIR + s); };
-  auto bar_pe_empty = [&](int s) { return bar0 + 8u * (2 * NPAIR + NPE + s); };
-  const uint32_t bar_x = bar0 + 8u * (2 * NPAIR + 2 * NPE);
+  auto bar_pair_empty = [&](int s) { return bar0 + 8u * (C::NPAIR + s); };
+  const uint32_t bar_pe_full = bar0 + 8u * (2 * C::NPAIR);
+  const uint32_t bar_pe_empty = bar_pe_full + 8u;
+  const uint32_t bar_x = bar_pe_full + 16u;
   const uint32_t bar_q_full = bar_x;
   const uint32_t bar_q_empty = bar_x + 8u;
   auto bar_s_full = [&](int i) { return bar_x + 8u * (2 + i); };
@@ -193,7 +253,7 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
   const uint32_t bar_p_full = bar_x + 8u * 6;
   const uint32_t bar_o_done = bar_x + 8u * 7;
   const uint32_t bar_o_free = bar_x + 8u * 8;
-  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + OFF_TMEMPTR);
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -213,14 +273,12 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     prefetch_tmap(&p.tm_qpe);
     prefetch_tmap(&p.tm_k);
     prefetch_tmap(&p.tm_kpe);
-    for (int s = 0; s < NPAIR; ++s) {
+    for (int s = 0; s < C::NPAIR; ++s) {
       mbar_init(bar_pair_full(s), 1);
       mbar_init(bar_pair_empty(s), p.CL);  // released by the PV MMAs of every CTA of the cluster
     }
-    for (int s = 0; s < NPE; ++s) {
-      mbar_init(bar_pe_full(s), 1);
-      mbar_init(bar_pe_empty(s), p.CL);
-    }
+    mbar_init(bar_pe_full, 1);
+    mbar_init(bar_pe_empty, p.CL);
     mbar_init(bar_q_full, 1);
     mbar_init(bar_q_empty, 1);
     for (int i = 0; i < 2; ++i) {
@@ -232,7 +290,7 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     mbar_init(bar_o_free, 4);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(smem_u32(tmem_ptr_smem));
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_ptr_smem));
   tc_fence_before();
   if (p.CL > 1) cluster_sync();  // peers' barriers initialised before any multicast / remote arrive
   else __syncthreads();
@@ -241,13 +299,13 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
 
   if (warp == 0) {
     // ================================ TMA producer ================================
-    // Block j of a segment = K_pe chunk (pe ring) + 4 pair slots, pair m = KV dims
-    // [128m, 128m+128) as two [128 keys x 64] SWIZZLE_128B boxes. The pair slots stay
-    // resident from S(j) to PV(j) (they are both the QK^T operand and V). With CL > 1, unit
-    // number u (pairs and pe counted separately) is loaded by CTA (u % CL) and multicast.
+    // Block j of a segment = four "pair" slots (KV dims [128m, 128m+128) as two
+    // [128 keys x 64] SWIZZLE_128B boxes) + the K_pe chunk. The pair slots stay resident from
+    // S(j) to PV(j) (they are both the QK^T operand and V). With CL > 1, unit number u (pairs
+    // and K_pe counted separately) is loaded by CTA (u % CL) and multicast.
     if (lane == 0) {
       const uint64_t pol_q = policy_evict_first();
-      const uint64_t pol_kv = policy_evict_first();  // streamed once (per head tile)
+      const uint64_t pol_kv = policy_evict_first();  // streamed once per head tile
       uint32_t pit = 0, eit = 0;
       int nseg = 0;
       SegIter si(p, part);
@@ -258,28 +316,27 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         if (p.CL > 1) tma_load_4d_mc(dst, m, fb, c0, c1, c2, c3, mc_mask, pol);
         else tma_load_4d(dst, m, fb, c0, c1, c2, c3, pol);
       };
+      auto load_pe = [&](int key0, int b) {
+        if (eit >= 1u) mbar_wait(bar_pe_empty, (eit - 1) & 1);
+        mbar_arrive_expect_tx(bar_pe_full, SLOT);
+        load((eit % p.CL) == rank, sPe, &p.tm_kpe, bar_pe_full, 0, kvh, key0, b, pol_kv);
+        ++eit;
+      };
       while (si.next(p, sg)) {
         if (nseg > 0) mbar_wait(bar_q_empty, (nseg - 1) & 1);  // previous segment's S MMAs done
-        mbar_arrive_expect_tx(bar_q_full, NKCH * QCH);
+        mbar_arrive_expect_tx(bar_q_full, NKCH * C::QCH);
 #pragma unroll 1
         for (int c = 0; c < DL / 64; ++c)
-          tma_load_4d(sQ + c * QCH, &p.tm_q, bar_q_full, c * 64, h0, 0, sg.b, pol_q);
-        tma_load_4d(sQ + (DL / 64) * QCH, &p.tm_qpe, bar_q_full, 0, h0, 0, sg.b, pol_q);
+          tma_load_4d(sQ + c * C::QCH, &p.tm_q, bar_q_full, c * 64, h0, 0, sg.b, pol_q);
+        tma_load_4d(sQ + (DL / 64) * C::QCH, &p.tm_qpe, bar_q_full, 0, h0, 0, sg.b, pol_q);
 #pragma unroll 1
         for (int jj = 0; jj < sg.n; ++jj) {
           const int key0 = (sg.k0 + jj) * BLK;
-          {  // K_pe chunk
-            const int s = eit % NPE;
-            if (eit >= (uint32_t)NPE) mbar_wait(bar_pe_empty(s), ((eit / NPE) - 1) & 1);
-            mbar_arrive_expect_tx(bar_pe_full(s), SLOT);
-            load((eit % p.CL) == rank, sPe + s * SLOT, &p.tm_kpe, bar_pe_full(s), 0, kvh, key0,
-                 sg.b, pol_kv);
-            ++eit;
-          }
+          if constexpr (C::PREFETCH) load_pe(key0, sg.b);  // S(j) starts with K_pe
 #pragma unroll 1
           for (int m = 0; m < NPAIRS_PER_BLK; ++m) {
-            const int s = pit % NPAIR;
-            if (pit >= (uint32_t)NPAIR) mbar_wait(bar_pair_empty(s), ((pit / NPAIR) - 1) & 1);
+            const int s = pit % C::NPAIR;
+            if (pit >= (uint32_t)C::NPAIR) mbar_wait(bar_pair_empty(s), ((pit / C::NPAIR) - 1) & 1);
             mbar_arrive_expect_tx(bar_pair_full(s), 2 * SLOT);
             const bool mine = (pit % p.CL) == rank;
             load(mine, sPair + s * 2 * SLOT, &p.tm_k, bar_pair_full(s), (2 * m) * 64, kvh, key0, sg.b,
@@ -288,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
                  key0, sg.b, pol_kv);
             ++pit;
           }
+          if constexpr (!C::PREFETCH) load_pe(key0, sg.b);  // S(j) ends with K_pe (slot = P^T)
         }
         ++nseg;
       }
@@ -295,9 +353,10 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     __syncwarp();
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
-    // Per block: S(j+1) part A (K_pe + pair 0, which fit in the free slots) -> PV(j) (frees the
-    // pair slots of block j) -> S(j+1) part B (pairs 1-3). The tensor core computes the next
-    // scores while softmax(j) runs.
+    // HC = 32: S(j+1) part A (K_pe, pair 0 = the prefetched slots) -> PV(j) (frees the pair
+    //          slots of block j) -> S(j+1) part B (pairs 1-3): the tensor core computes the
+    //          next scores while softmax(j) runs.
+    // HC = 64: S(j) (pairs 0-3, then K_pe) -> PV(j) -> S(j+1) ...
     if (lane == 0) {
       constexpr uint32_t FMT = BF16 ? 1u : 0u;
       // S^T = Khat Qhat^T: A = Khat (K-major), B = Qhat (K-major), M=128 keys, N=HC heads
@@ -305,85 +364,109 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
       // O^T += V^T P^T: A = V^T (MN-major: dv contiguous), B = P^T (MN-major: heads
       // contiguous), M=128 dv, N=HC heads, K=128 keys
       constexpr uint32_t IDESC_PV = make_idesc_f16(FMT, 128, HC, 1, 1, 0);
-      uint32_t pit = 0, eit = 0;  // pair / pe ring positions (same sequence as the producer)
+      uint32_t pit = 0, eit = 0;  // pair / K_pe positions (same sequence as the producer)
       uint32_t gb = 0;            // global block counter
       int nseg = 0;
       SegIter si(p, part);
       Seg sg;
-      // S^T(gs) += Khat chunk(s) . Qhat chunk(c)
+      // S^T(gs) += Khat chunk . Qhat chunk(c)
       auto s_chunk = [&](uint32_t sb, uint32_t a0, int c, bool first) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_f16_ss(tmem_base + TM_S + sb * HC, make_sdesc(a0 + kk * 32, 16, 1024, 2),
-                     make_sdesc(sQ + c * QCH + kk * 32, 16, 1024, 2), IDESC_S,
+          mma_f16_ss(tmem_base + C::TM_S + sb * HC, make_sdesc(a0 + kk * 32, 16, 1024, 2),
+                     make_sdesc(sQ + c * C::QCH + kk * 32, 16, 1024, 2), IDESC_S,
                      (first && kk == 0) ? 0u : 1u);
       };
-      auto s_pe = [&](uint32_t sb) {  // K_pe chunk (first MMAs of S(gs))
-        const int s = eit % NPE;
-        mbar_wait(bar_pe_full(s), (eit / NPE) & 1);
+      auto s_pe = [&](uint32_t sb, bool first) {  // K_pe chunk
+        mbar_wait(bar_pe_full, eit & 1);
         tc_fence_after();
-        s_chunk(sb, sPe + s * SLOT, DL / 64, true);
-        if (p.CL > 1) mma_commit_mc(bar_pe_empty(s), mc_mask);
-        else mma_commit(bar_pe_empty(s));
+        s_chunk(sb, sPe, DL / 64, first);
+        if constexpr (C::PREFETCH) {  // (HC = 64: the slot is released after PV, as P^T)
+          if (p.CL > 1) mma_commit_mc(bar_pe_empty, mc_mask);
+          else mma_commit(bar_pe_empty);
+        }
         ++eit;
       };
-      auto s_pair = [&](uint32_t sb, uint32_t pos, int m) {
-        const int s = pos % NPAIR;
-        mbar_wait(bar_pair_full(s), (pos / NPAIR) & 1);
+      auto s_pair = [&](uint32_t sb, uint32_t pos, int m, bool first) {
+        const int s = pos % C::NPAIR;
+        mbar_wait(bar_pair_full(s), (pos / C::NPAIR) & 1);
         tc_fence_after();
-        s_chunk(sb, sPair + s * 2 * SLOT, 2 * m, false);
+        s_chunk(sb, sPair + s * 2 * SLOT, 2 * m, first);
         s_chunk(sb, sPair + s * 2 * SLOT + SLOT, 2 * m + 1, false);
       };
       auto s_begin = [&](uint32_t gs) {
         if (gs >= 2) mbar_wait(bar_s_free(gs & 1), ((gs - 2) >> 1) & 1);
         tc_fence_after();
       };
+      auto pv = [&](uint32_t g, uint32_t pos, bool first_blk) {
+        mbar_wait(bar_p_full, g & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int m = 0; m < NPAIRS_PER_BLK; ++m) {
+          const int s = (pos + m) % C::NPAIR;
+          const uint32_t a0 = sPair + s * 2 * SLOT;
+#pragma unroll
+          for (int kk = 0; kk < BLK / 16; ++kk) {
+            // A: V^T MN-major SW128, 16 keys = 16 rows of 128 B; LBO = 16 KB to the second
+            // 64-wide dv atom of the pair. B: P^T MN-major, 16 keys = 16 rows of P_ROW bytes.
+            mma_f16_ss(tmem_base + C::TM_O + m * HC, make_sdesc(a0 + kk * 2048, SLOT, 1024, 2),
+                       make_sdesc(sP + kk * 16 * C::P_ROW, 4096, 8 * C::P_ROW, C::P_LAYOUT),
+                       IDESC_PV, (!first_blk || kk > 0) ? 1u : 0u);
+          }
+          if (p.CL > 1) mma_commit_mc(bar_pair_empty(s), mc_mask);
+          else mma_commit(bar_pair_empty(s));
+        }
+        if constexpr (!C::PREFETCH) {  // P^T read: the K_pe slot may be refilled
+          if (p.CL > 1) mma_commit_mc(bar_pe_empty, mc_mask);
+          else mma_commit(bar_pe_empty);
+        }
+        mma_commit(bar_o_done);
+      };
       while (si.next(p, sg)) {
         mbar_wait(bar_q_full, nseg & 1);
         tc_fence_after();
         const uint32_t pit0 = pit;  // pair position of block 0 of this segment, pair 0
-        // S(0), whole
-        s_begin(gb);
-        s_pe(gb & 1);
+        if constexpr (C::PREFETCH) {
+          // S(0), whole
+          s_begin(gb);
+          s_pe(gb & 1, true);
 #pragma unroll 1
-        for (int m = 0; m < NPAIRS_PER_BLK; ++m) s_pair(gb & 1, pit0 + m, m);
-        mma_commit(bar_s_full(gb & 1));
-        if (sg.n == 1) mma_commit(bar_q_empty);
+          for (int m = 0; m < NPAIRS_PER_BLK; ++m) s_pair(gb & 1, pit0 + m, m, false);
+          mma_commit(bar_s_full(gb & 1));
+          if (sg.n == 1) mma_commit(bar_q_empty);
 #pragma unroll 1
-        for (int jj = 0; jj < sg.n; ++jj) {
-          const uint32_t g = gb + jj;
-          const uint32_t pos = pit0 + NPAIRS_PER_BLK * jj;  // pair 0 of block jj
-          const bool more = jj + 1 < sg.n;
-          if (more) {  // S(j+1) part A
-            s_begin(g + 1);
-            s_pe((g + 1) & 1);
-            s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK, 0);
-          }
-          // PV(j)
-          if (jj == 0 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
-          mbar_wait(bar_p_full, g & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int m = 0; m < NPAIRS_PER_BLK; ++m) {
-            const int s = (pos + m) % NPAIR;
-            const uint32_t a0 = sPair + s * 2 * SLOT;
-#pragma unroll
-            for (int kk = 0; kk < BLK / 16; ++kk) {
-              // A: V^T MN-major SW128, 16 keys = 16 rows of 128 B; LBO = 16 KB to the second
-              // 64-wide dv atom of the pair. B: P^T MN-major SW64, 16 keys = 16 rows of 64 B.
-              mma_f16_ss(tmem_base + TM_O + m * HC, make_sdesc(a0 + kk * 2048, SLOT, 1024, 2),
-                         make_sdesc(sP + kk * 1024, 4096, 512, 4), IDESC_PV,
-                         (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int jj = 0; jj < sg.n; ++jj) {
+            const uint32_t g = gb + jj;
+            const uint32_t pos = pit0 + NPAIRS_PER_BLK * jj;  // pair 0 of block jj
+            const bool more = jj + 1 < sg.n;
+            if (more) {  // S(j+1) part A
+              s_begin(g + 1);
+              s_pe((g + 1) & 1, true);
+              s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK, 0, false);
             }
-            if (p.CL > 1) mma_commit_mc(bar_pair_empty(s), mc_mask);
-            else mma_commit(bar_pair_empty(s));
-          }
-          mma_commit(bar_o_done);
-          if (more) {  // S(j+1) part B
+            if (jj == 0 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
+            pv(g, pos, jj == 0);
+            if (more) {  // S(j+1) part B
 #pragma unroll 1
-            for (int m = 1; m < NPAIRS_PER_BLK; ++m) s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK + m, m);
-            mma_commit(bar_s_full((g + 1) & 1));
-            if (jj + 2 == sg.n) mma_commit(bar_q_empty);
+              for (int m = 1; m < NPAIRS_PER_BLK; ++m)
+                s_pair((g + 1) & 1, pos + NPAIRS_PER_BLK + m, m, false);
+              mma_commit(bar_s_full((g + 1) & 1));
+              if (jj + 2 == sg.n) mma_commit(bar_q_empty);
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int jj = 0; jj < sg.n; ++jj) {
+            const uint32_t g = gb + jj;
+            const uint32_t pos = pit0 + NPAIRS_PER_BLK * jj;
+            s_begin(g);
+#pragma unroll 1
+            for (int m = 0; m < NPAIRS_PER_BLK; ++m) s_pair(g & 1, pos + m, m, m == 0);
+            s_pe(g & 1, false);
+            mma_commit(bar_s_full(g & 1));
+            if (jj + 1 == sg.n) mma_commit(bar_q_empty);
+            if (jj == 0 && nseg > 0) mbar_wait(bar_o_free, (nseg - 1) & 1);  // O^T read out
+            pv(g, pos, jj == 0);
           }
         }
         pit += NPAIRS_PER_BLK * sg.n;
@@ -404,8 +487,10 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     SegIter si(p, part);
     Seg sg;
     while (si.next(p, sg)) {
-      float m = -INFINITY;  // running max (log2 units) of head `lane` (same in all 4 warps)
-      float lpart[HC];      // this key-thread's share of l for every head
+      float m[R];          // running max (log2 units) of heads lane*R + i (same in all 4 warps)
+      float lpart[HC];     // this key-thread's share of l for every head
+#pragma unroll
+      for (int i = 0; i < R; ++i) m[i] = -INFINITY;
 #pragma unroll
       for (int h = 0; h < HC; ++h) lpart[h] = 0.f;
 #pragma unroll 1
@@ -415,7 +500,10 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         mbar_wait(bar_s_full(sb), (gs >> 1) & 1);
         tc_fence_after();
         float s[HC];
-        tmem_ld32(tmem_base + lane_off + TM_S + sb * HC, *reinterpret_cast<uint32_t(*)[32]>(s));
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc)
+          tmem_ld32(tmem_base + lane_off + C::TM_S + sb * HC + cc * 32,
+                    *reinterpret_cast<uint32_t(*)[32]>(s + cc * 32));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -425,41 +513,36 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
 #pragma unroll
           for (int h = 0; h < HC; ++h) s[h] = -INFINITY;
         }
-        // per-head (column) max over the 128 keys: transposed butterfly inside the warp
-        // (lane l ends with column l), then the 4 warps through smem (T.reduce_max)
-        float v[HC];
+        // per-head (column) max over the 128 keys: transposed butterfly inside the warp,
+        // then the 4 warps through smem (T.reduce_max)
+        float v[HC / 2];
+        col_reduce<HC, true>(s, v, lane);
+        float* rb = red + (gs & 1) * 4 * HC;
 #pragma unroll
-        for (int h = 0; h < HC; ++h) v[h] = s[h];
-#pragma unroll
-        for (int w = HC / 2; w >= 1; w >>= 1) {
-          const bool up = (lane & w) != 0;
-#pragma unroll
-          for (int i = 0; i < w; ++i) {
-            const float send = up ? v[i] : v[i + w];
-            const float keep = up ? v[i + w] : v[i];
-            v[i] = fmaxf(keep, __shfl_xor_sync(FULL, send, w));
-          }
-        }
-        float* rb = red + (gs & 1) * 128;
-        rb[q4 * 32 + lane] = v[0];
+        for (int i = 0; i < R; ++i) rb[q4 * HC + lane * R + i] = v[i];
         named_bar_sync(1, 128);
-        const float mx = fmaxf(fmaxf(rb[lane], rb[32 + lane]), fmaxf(rb[64 + lane], rb[96 + lane]));
-        const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
-        const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        const float alpha = ex2(m - m_use);  // scores_scale; 0 on the first block
+        float m_new[R], m_use[R], alpha[R];
+        bool any_resc = false;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int hh = lane * R + i;
+          const float mx = fmaxf(fmaxf(rb[hh], rb[HC + hh]), fmaxf(rb[2 * HC + hh], rb[3 * HC + hh]));
+          const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
+          m_new[i] = (mxs > m[i] + RESCALE_LOG2) ? mxs : m[i];  // conditional rescale
+          m_use[i] = (m_new[i] == -INFINITY) ? 0.f : m_new[i];
+          alpha[i] = ex2(m[i] - m_use[i]);  // scores_scale; 0 on the first block
+          any_resc |= alpha[i] != 1.f;
+        }
         // p = exp2(s c - m_head), l partial sums from the unrounded p (R8)
         uint32_t pk[HC / 2];
-        const bool resc = __any_sync(FULL, alpha != 1.f);
+        const bool resc = __any_sync(FULL, any_resc);
 #pragma unroll
         for (int h = 0; h < HC; h += 2) {
-          const float m0 = __shfl_sync(FULL, m_use, h);
-          const float m1 = __shfl_sync(FULL, m_use, h + 1);
-          const float p0 = ex2(fmaf(s[h], c, -m0));
-          const float p1 = ex2(fmaf(s[h + 1], c, -m1));
+          const float p0 = ex2(fmaf(s[h], c, -head_val<R>(m_use, h)));
+          const float p1 = ex2(fmaf(s[h + 1], c, -head_val<R>(m_use, h + 1)));
           if (resc) {
-            lpart[h] *= __shfl_sync(FULL, alpha, h);
-            lpart[h + 1] *= __shfl_sync(FULL, alpha, h + 1);
+            lpart[h] *= head_val<R>(alpha, h);
+            lpart[h + 1] *= head_val<R>(alpha, h + 1);
           }
           lpart[h] += p0;
           lpart[h + 1] += p1;
@@ -472,89 +555,100 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
           tc_fence_after();
           float al[HC];
 #pragma unroll
-          for (int h = 0; h < HC; ++h) al[h] = __shfl_sync(FULL, alpha, h);
+          for (int h = 0; h < HC; ++h) al[h] = head_val<R>(alpha, h);
 #pragma unroll 1
           for (int mm = 0; mm < DL / 128; ++mm) {
-            uint32_t ov[32];
-            tmem_ld32(tmem_base + lane_off + TM_O + mm * HC, ov);
-            tmem_ld_wait();
 #pragma unroll
-            for (int h = 0; h < HC; ++h) ov[h] = __float_as_uint(__uint_as_float(ov[h]) * al[h]);
-            tmem_st32(tmem_base + lane_off + TM_O + mm * HC, ov);
+            for (int cc = 0; cc < R; ++cc) {
+              uint32_t ov[32];
+              const uint32_t ta = tmem_base + lane_off + C::TM_O + mm * HC + cc * 32;
+              tmem_ld32(ta, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int h = 0; h < 32; ++h)
+                ov[h] = __float_as_uint(__uint_as_float(ov[h]) * al[cc * 32 + h]);
+              tmem_st32(ta, ov);
+            }
           }
           tmem_st_wait();
         }
-        // P^T row (this key, 32 heads = 64 B) -> smem, MN-major SWIZZLE_64B:
-        // 16-B unit u of row r lands at u ^ ((r >> 1) & 3)
-        const uint32_t prow = sP + row * 64;
+        // P^T row (this key, HC heads) -> smem, MN-major: HC = 32 SWIZZLE_64B (16-B unit u of
+        // row r at u ^ ((r >> 1) & 3)), HC = 64 SWIZZLE_128B (unit u at u ^ (r & 7))
+        const uint32_t prow = sP + row * C::P_ROW;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          st_shared_v4(prow + ((u ^ ((row >> 1) & 3)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
-                       pk[4 * u + 3]);
+        for (int u = 0; u < HC / 8; ++u) {
+          const uint32_t pu = HC == 32 ? (u ^ ((row >> 1) & 3)) : (u ^ (row & 7));
+          st_shared_v4(prow + (pu << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_full);
-        m = m_new;
+#pragma unroll
+        for (int i = 0; i < R; ++i) m[i] = m_new[i];
       }
       // ---- epilogue: l = sum of the partial sums, O = O^T / l, LSE
       const uint32_t glast = gb + sg.n - 1;
       mbar_wait(bar_o_done, glast & 1);
       tc_fence_after();
       {
-        float v[HC];
+        float v[HC / 2];
+        col_reduce<HC, false>(lpart, v, lane);
 #pragma unroll
-        for (int h = 0; h < HC; ++h) v[h] = lpart[h];
-#pragma unroll
-        for (int w = HC / 2; w >= 1; w >>= 1) {
-          const bool up = (lane & w) != 0;
-#pragma unroll
-          for (int i = 0; i < w; ++i) {
-            const float send = up ? v[i] : v[i + w];
-            const float keep = up ? v[i + w] : v[i];
-            v[i] = keep + __shfl_xor_sync(FULL, send, w);
-          }
-        }
-        redl[q4 * 32 + lane] = v[0];
+        for (int i = 0; i < R; ++i) redl[q4 * HC + lane * R + i] = v[i];
       }
       named_bar_sync(1, 128);
-      const float L = (redl[lane] + redl[32 + lane]) + (redl[64 + lane] + redl[96 + lane]);
-      const float m_fin = (m == -INFINITY) ? 0.f : m;
-      const float inv = (L > 0.f) ? 1.f / L : 0.f;
-      const float lse2 = (L > 0.f) ? m_fin + __log2f(L) : -INFINITY;
+      float inv[R], lse2[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int hh = lane * R + i;
+        const float L = (redl[hh] + redl[HC + hh]) + (redl[2 * HC + hh] + redl[3 * HC + hh]);
+        const float m_fin = (m[i] == -INFINITY) ? 0.f : m[i];
+        inv[i] = (L > 0.f) ? 1.f / L : 0.f;
+        lse2[i] = (L > 0.f) ? m_fin + __log2f(L) : -INFINITY;
+      }
       float iv[HC];
 #pragma unroll
-      for (int h = 0; h < HC; ++h) iv[h] = __shfl_sync(FULL, inv, h);
+      for (int h = 0; h < HC; ++h) iv[h] = head_val<R>(inv, h);
       const size_t wslot = ((size_t)(hgi * p.P + part) * 2 + sg.slot);
 #pragma unroll 1
       for (int mm = 0; mm < DL / 128; ++mm) {
-        uint32_t ov[32];
-        tmem_ld32(tmem_base + lane_off + TM_O + mm * HC, ov);
-        tmem_ld_wait();
         const int dv = mm * 128 + row;
-        if (!sg.partial) {
-          using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
-          T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)sg.b * p.H + h0) * DL + dv;
 #pragma unroll
-          for (int h = 0; h < HC; ++h) {
-            if (h < nvalid) {
-              const float x = __uint_as_float(ov[h]) * iv[h];
-              if constexpr (BF16) ob[(size_t)h * DL] = __float2bfloat16_rn(x);
-              else ob[(size_t)h * DL] = __float2half_rn(x);
+        for (int cc = 0; cc < R; ++cc) {
+          uint32_t ov[32];
+          tmem_ld32(tmem_base + lane_off + C::TM_O + mm * HC + cc * 32, ov);
+          tmem_ld_wait();
+          if (!sg.partial) {
+            using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+            T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)sg.b * p.H + h0) * DL + dv;
+#pragma unroll
+            for (int h = 0; h < 32; ++h) {
+              const int hh = cc * 32 + h;
+              if (hh < nvalid) {
+                const float x = __uint_as_float(ov[h]) * iv[hh];
+                if constexpr (BF16) ob[(size_t)hh * DL] = __float2bfloat16_rn(x);
+                else ob[(size_t)hh * DL] = __float2half_rn(x);
+              }
             }
-          }
-        } else {
-          float* wo = p.ws_o + wslot * HC * DL + dv;
+          } else {
+            float* wo = p.ws_o + wslot * HC * DL + dv;
 #pragma unroll
-          for (int h = 0; h < HC; ++h) wo[(size_t)h * DL] = __uint_as_float(ov[h]) * iv[h];
+            for (int h = 0; h < 32; ++h)
+              wo[(size_t)(cc * 32 + h) * DL] = __uint_as_float(ov[h]) * iv[cc * 32 + h];
+          }
         }
       }
       if (q4 == 0) {
-        if (!sg.partial) {
-          if (p.lse != nullptr && lane < nvalid)
-            p.lse[(size_t)sg.b * p.H + h0 + lane] = lse2 * 0.69314718055994531f;
-        } else {
-          p.ws_lse[wslot * HC + lane] = lse2;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int hh = lane * R + i;
+          if (!sg.partial) {
+            if (p.lse != nullptr && hh < nvalid)
+              p.lse[(size_t)sg.b * p.H + h0 + hh] = lse2[i] * 0.69314718055994531f;
+          } else {
+            p.ws_lse[wslot * HC + hh] = lse2[i];
+          }
         }
       }
       tc_fence_before();
@@ -571,7 +665,7 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -618,12 +712,13 @@ __global__ void __launch_bounds__(1024) tl_mla_meta_kernel(const int* seqlens, i
 }
 
 // Merge the partial (O, lse) pieces of split batches; write zeros / -inf for empty ones.
-// Grid: (B, Hkv * T); 256 threads: warp w handles heads w, w+8, w+16, w+24 of the tile.
+// Grid: (B, Hkv * T); 256 threads: warp w handles heads w, w+8, ... of the tile.
 template <bool BF16>
 __global__ void __launch_bounds__(256) tl_mla_combine_kernel(const __grid_constant__ MlaParams p) {
   const int b = blockIdx.x;
   const int hgi = blockIdx.y;
   const int kvh = hgi / p.T, t = hgi % p.T;
+  const int HC = p.HC;
   const int h0 = kvh * p.g + t * HC;
   const int nvalid = min(HC, p.g - t * HC);
   const long long W = p.cum[p.B];

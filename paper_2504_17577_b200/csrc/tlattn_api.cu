@@ -395,7 +395,7 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
 // ------------------------------------------------------------------ MLA decode
 namespace {
 struct MlaPlan {
-  int T, NHG, P, CL;
+  int HC, T, NHG, P, CL;
   size_t off_lse, off_o, bytes;
 };
 
@@ -416,7 +416,13 @@ int mla_max_clusters(int dev, int cl, int sm_count);
 MlaPlan plan_mla(int B, int H, int Hkv, int dev, int sm_count) {
   MlaPlan pl;
   const int g = H / Hkv;
-  pl.T = (g + mla::HC - 1) / mla::HC;
+  // 64-head tiles read the latent cache half as often as 32-head tiles
+  pl.HC = g >= 64 ? 64 : 32;
+  if (const char* e = std::getenv("TLATTN_MLA_HC")) {  // A/B experiments only
+    const int v = std::atoi(e);
+    if (v == 32 || v == 64) pl.HC = v;
+  }
+  pl.T = (g + pl.HC - 1) / pl.HC;
   pl.NHG = Hkv * pl.T;
   pl.CL = mla_cluster_size(pl.T);
   // all CTAs co-resident (one per SM): clusters that fit / cluster groups = partitions
@@ -424,8 +430,8 @@ MlaPlan plan_mla(int B, int H, int Hkv, int dev, int sm_count) {
   pl.P = mla_max_clusters(dev, pl.CL, sm_count) / groups;
   if (pl.P < 1) pl.P = 1;
   pl.off_lse = al256((size_t)(B + 1) * 4);
-  pl.off_o = pl.off_lse + al256((size_t)pl.NHG * pl.P * 2 * mla::HC * 4);
-  pl.bytes = pl.off_o + (size_t)pl.NHG * pl.P * 2 * mla::HC * mla::DL * 4;
+  pl.off_o = pl.off_lse + al256((size_t)pl.NHG * pl.P * 2 * pl.HC * 4);
+  pl.bytes = pl.off_o + (size_t)pl.NHG * pl.P * 2 * pl.HC * mla::DL * 4;
   return pl;
 }
 
@@ -442,15 +448,19 @@ bool encode_4d(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void
 std::mutex g_mla_mu;
 int g_mla_clusters[kMaxDevices][5] = {};
 
+template <int HC, bool BF16>
+bool mla_attr_one() {
+  auto k = mla::tl_mla_decode_kernel<HC, BF16>;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              mla::Cfg<HC>::SMEM_BYTES) == cudaSuccess &&
+         cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+}
+
 bool mla_smem_attr(int dev) {
   static bool done[kMaxDevices] = {};
   if (done[dev]) return true;
-  if (cudaFuncSetAttribute(mla::tl_mla_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           mla::SMEM_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           mla::SMEM_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-      cudaFuncSetAttribute(mla::tl_mla_decode_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+  if (!mla_attr_one<32, true>() || !mla_attr_one<32, false>() || !mla_attr_one<64, true>() ||
+      !mla_attr_one<64, false>()) {
     cudaGetLastError();
     return false;
   }
@@ -466,7 +476,7 @@ int mla_max_clusters(int dev, int cl, int sm_count) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl * (sm_count / cl), 1, 1);
     cfg.blockDim = dim3(mla::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = mla::SMEM_BYTES;
+    cfg.dynamicSmemBytes = mla::Cfg<64>::SMEM_BYTES;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
@@ -475,7 +485,8 @@ int mla_max_clusters(int dev, int cl, int sm_count) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int c = 0;
-    if (cudaOccupancyMaxActiveClusters(&c, mla::tl_mla_decode_kernel<true>, &cfg) == cudaSuccess && c > 0)
+    if (cudaOccupancyMaxActiveClusters(&c, mla::tl_mla_decode_kernel<64, true>, &cfg) == cudaSuccess &&
+        c > 0)
       n = c;
     cudaGetLastError();
   }
@@ -483,7 +494,7 @@ int mla_max_clusters(int dev, int cl, int sm_count) {
   return n;
 }
 
-template <bool BF16>
+template <int HC, bool BF16>
 int launch_mla(const mla::MlaParams& prm, int dev, int B, const int* seqlens, int Skv,
                cudaStream_t stream) {
   {
@@ -495,7 +506,7 @@ int launch_mla(const mla::MlaParams& prm, int dev, int B, const int* seqlens, in
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prm.Hkv * prm.T * prm.P, 1, 1);
   cfg.blockDim = dim3(mla::THREADS, 1, 1);
-  cfg.dynamicSmemBytes = mla::SMEM_BYTES;
+  cfg.dynamicSmemBytes = mla::Cfg<HC>::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -504,7 +515,7 @@ int launch_mla(const mla::MlaParams& prm, int dev, int B, const int* seqlens, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, mla::tl_mla_decode_kernel<BF16>, prm) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&cfg, mla::tl_mla_decode_kernel<HC, BF16>, prm) != cudaSuccess) {
     cudaGetLastError();
     return TL_ERR_CUDA;
   }
@@ -549,8 +560,8 @@ extern "C" int tl_mla_decode(const void* q, const void* q_pe, const void* kv, co
   mla::MlaParams prm;
   std::memset(&prm, 0, sizeof(prm));
   const cuuint64_t HH = (cuuint64_t)H, BB = (cuuint64_t)B, SS = (cuuint64_t)Skv, GG = (cuuint64_t)Hkv;
-  if (!encode_4d(enc, &prm.tm_q, q, dtype, {(cuuint64_t)mla::DL, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
-      !encode_4d(enc, &prm.tm_qpe, q_pe, dtype, {(cuuint64_t)mla::DR, HH, 1, BB}, {64, mla::HC, 1, 1}) ||
+  if (!encode_4d(enc, &prm.tm_q, q, dtype, {(cuuint64_t)mla::DL, HH, 1, BB}, {64, (cuuint32_t)pl.HC, 1, 1}) ||
+      !encode_4d(enc, &prm.tm_qpe, q_pe, dtype, {(cuuint64_t)mla::DR, HH, 1, BB}, {64, (cuuint32_t)pl.HC, 1, 1}) ||
       !encode_4d(enc, &prm.tm_k, kv, dtype, {(cuuint64_t)mla::DL, GG, SS, BB}, {64, 1, mla::BLK, 1}) ||
       !encode_4d(enc, &prm.tm_kpe, k_pe, dtype, {(cuuint64_t)mla::DR, GG, SS, BB}, {64, 1, mla::BLK, 1}))
     return TL_ERR_CUDA;
@@ -569,12 +580,16 @@ extern "C" int tl_mla_decode(const void* q, const void* q_pe, const void* kv, co
   prm.T = pl.T;
   prm.P = pl.P;
   prm.CL = pl.CL;
+  prm.HC = pl.HC;
   prm.c_log2 = std::fabs(scale) * 1.4426950408889634f;
   if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;  // scale = 0: see tl_attn_fwd
   prm.neg = scale < 0.f ? 1 : 0;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  rc = dtype == TL_DTYPE_BF16 ? launch_mla<true>(prm, dev, B, seqlens, Skv, st)
-                              : launch_mla<false>(prm, dev, B, seqlens, Skv, st);
+  const bool bf = dtype == TL_DTYPE_BF16;
+  if (pl.HC == 64)
+    rc = bf ? launch_mla<64, true>(prm, dev, B, seqlens, Skv, st) : launch_mla<64, false>(prm, dev, B, seqlens, Skv, st);
+  else
+    rc = bf ? launch_mla<32, true>(prm, dev, B, seqlens, Skv, st) : launch_mla<32, false>(prm, dev, B, seqlens, Skv, st);
   if (rc == TL_OK) g_last_launches = 3;
   return rc;
 }

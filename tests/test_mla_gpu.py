@@ -55,6 +55,8 @@ def run_and_check(B, H, Hkv, Skv, dtype, seqlens=None, scale=None, seed=7, batch
     (4, 40, 1, 777, F16, "ragged"),     # 40 heads: a full and a partial head tile
     (5, 128, 1, 2048, F16, "edge"),     # n_b in {0, 1, 127, 128, 129}
     (16, 16, 1, 1024, BF, "ragged"),    # TP8-style head count
+    (2, 96, 1, 600, F16, "ragged"),     # 64-head tiles: one full, one with 32 valid heads
+    (3, 256, 2, 700, BF, "ragged"),     # 64-head tiles, GQA (2 kv heads x 2 tiles)
 ])
 def test_mla_parity_small(B, H, Hkv, Skv, dtype, kind):
     if kind == "ragged":
@@ -72,6 +74,13 @@ def test_mla_scale_values(scale):
     # scale = 0: uniform weights (O = mean of kv, LSE = ln n); negative: Qhat negated in the
     # instruction descriptor; 0.3: sharp softmax (rescales across blocks)
     run_and_check(2, 64, 1, 700, BF, gen_seqlens(2, 700, 5), scale=scale, label=f"scale {scale}")
+
+
+@pytest.mark.parametrize("hc", ["32", "64"])
+def test_mla_head_tile_widths_agree(hc, monkeypatch):
+    # the same problem through 32-head and 64-head tiles (TLATTN_MLA_HC, read per call)
+    monkeypatch.setenv("TLATTN_MLA_HC", hc)
+    run_and_check(2, 128, 1, 900, BF, gen_seqlens(2, 900, 8), label=f"HC={hc}")
 
 
 def test_mla_deterministic_and_zero_length():
