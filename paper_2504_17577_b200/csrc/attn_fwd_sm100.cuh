@@ -48,8 +48,9 @@ struct AttnParams {
   int causal;
   float c_log2;      // |scale| * log2(e)
   int neg;           // scale < 0: negate A (= Q) in the QK^T instruction descriptor
-  int n_mblk;        // ceil(Sq / 256)
+  int n_mblk;        // ceil(Sq / unit rows)
   int n_units;       // B * Hq * n_mblk
+  int unit_tiles;    // CTA-pair kernel: query tiles (of 256 rows) per unit, 2 or 1 (short Sq)
   unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
 };
 

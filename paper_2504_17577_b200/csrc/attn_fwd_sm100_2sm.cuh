@@ -39,7 +39,8 @@ struct KCfg2 {
   static constexpr int SMEM_BYTES = SMEM_USED + 1024;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
   static constexpr uint32_t TMEM_O = 2 * BN;
-  static constexpr int UNIT_ROWS = 2 * TILES * BM;  // 512 query rows per CTA pair
+  static constexpr int UNIT_ROWS = 2 * TILES * BM;  // 512 query rows per CTA pair (256 in
+                                                    // the short-sequence mode)
 };
 
 // K/V blocks a 256-row tile starting at r0 visits (causal tile skipping on the pair tile)
@@ -55,19 +56,21 @@ __device__ __forceinline__ int tile_nblocks_rows(int r0, int rows, const AttnPar
 
 struct Unit2 {
   int b, h, hkv, r0, n0, n1;
+  int tiles;  // query tiles this unit owns (2, or 1 in the short-sequence mode)
 };
 
 __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
   Unit2 U;
-  const int mb_i = u % p.n_mblk;  // n_mblk = ceil(Sq / 512) for this kernel
+  const int mb_i = u % p.n_mblk;  // n_mblk = ceil(Sq / (256 * unit_tiles)) for this kernel
   const int bh = u / p.n_mblk;
   U.h = bh % p.Hq;
   U.b = bh / p.Hq;
   const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
   U.hkv = U.h / (p.Hq / p.Hkv);  // GQA grouping
-  U.r0 = m_blk * KCfg2::UNIT_ROWS;
+  U.tiles = p.unit_tiles;
+  U.r0 = m_blk * (2 * BM) * p.unit_tiles;
   U.n0 = tile_nblocks_rows(U.r0, 2 * BM, p);
-  U.n1 = tile_nblocks_rows(U.r0 + 2 * BM, 2 * BM, p);
+  U.n1 = p.unit_tiles == 2 ? tile_nblocks_rows(U.r0 + 2 * BM, 2 * BM, p) : 0;
   return U;
 }
 
@@ -153,7 +156,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
           if (k >= 1) mbar_wait(bar_q_empty, (k - 1) & 1);
           if (leader) {
             uint32_t qbytes = 0;
-            for (int t = 0; t < TILES; ++t)
+            for (int t = 0; t < U.tiles; ++t)
               for (int c = 0; c < 2; ++c)
                 if (U.r0 + 256 * t + 128 * c < p.Sq) qbytes += C::Q_TILE_BYTES;
             mbar_arrive_expect_tx(bar_q_full, qbytes);
@@ -161,7 +164,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
 #pragma unroll
           for (int t = 0; t < TILES; ++t) {
             const int rq = U.r0 + 256 * t + 128 * (int)rank;
-            if (rq < p.Sq) {
+            if (t < U.tiles && rq < p.Sq) {
 #pragma unroll
               for (int c = 0; c < D / 64; ++c)
                 tma_load_4d_2sm(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, lead_q_full,
@@ -310,6 +313,15 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
 #else
       const int nt = t ? U.n1 : U.n0;
 #endif
+      if (t >= U.tiles) {  // short-sequence mode: this warpgroup's tile is not in the unit
+        mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+        const int nxt = clc_query(sSched + 16 * (k & 1));
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_sched_empty(k & 1), 0));
+        if (nxt < 0) break;
+        unit = nxt >> 1;
+        continue;
+      }
       const int row = U.r0 + 256 * t + 128 * (int)rank + lr;
       const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
       float m = -INFINITY;

@@ -193,7 +193,19 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
   // (-inf) still map to exp2(-inf) = 0 in the kernel's single exp path; with |s| << 1e28
   // every allowed p is exactly 1 and LSE = ln|J| up to ~1e-28.
   if (prm.c_log2 == 0.f) prm.c_log2 = 1e-30f;
-  const int unit_rows = pair ? KCfg2::UNIT_ROWS : TILES * BM;
+  // Short-sequence mode (the paper's "dynamic parameters", and its small-S point,
+  // P:L362): when the 512-row pair units would fill at most half of the SM pairs, units
+  // shrink to one 256-row tile so twice as many pairs work (Table 3 FA0/FA1 shapes).
+  prm.unit_tiles = 2;
+  if (pair) {
+    const long long units512 = (long long)B * Hq * ((Sq + 511) / 512);
+    if (2 * units512 <= di->sm_count / 2) prm.unit_tiles = 1;
+    if (const char* e = std::getenv("TLATTN_UNIT_TILES")) {  // A/B experiments only
+      const int v = std::atoi(e);
+      if (v == 1 || v == 2) prm.unit_tiles = v;
+    }
+  }
+  const int unit_rows = pair ? 2 * BM * prm.unit_tiles : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
   prm.n_units = B * Hq * prm.n_mblk;  // bounded in validate()
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the

@@ -45,6 +45,23 @@ def test_parity_small(B, Hq, Hkv, Sq, Skv, D, dtype, causal):
     print(stats)
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,Sq,Skv,causal", [
+    (1, 32, 32, 512, 512, True),     # Table 3 FA0 shape (the mode's own trigger)
+    (1, 32, 32, 512, 512, False),    # Table 3 FA1 shape
+    (2, 4, 2, 300, 300, True),       # ragged, GQA
+    (1, 3, 1, 700, 900, True),       # Sq < Skv, ragged, odd unit count
+    (1, 2, 2, 900, 600, False),      # Sq > Skv
+])
+@pytest.mark.parametrize("tiles", ["1", "2"])
+def test_pair_kernel_unit_modes(B, Hq, Hkv, Sq, Skv, causal, tiles, monkeypatch):
+    """CTA-pair kernel with 512-row units (2 tiles) and the short-sequence 256-row units
+    (TLATTN_UNIT_TILES forces the mode; read per call): same parity bar on every row."""
+    monkeypatch.setenv("TLATTN_UNIT_TILES", tiles)
+    q, k, v = gen(B, Hq, Hkv, Sq, Skv, 128, BF, 5 + Sq)
+    check_against_oracle(q, k, v, causal, default_scale(128),
+                         label=f"tiles={tiles} B{B} H{Hq}/{Hkv} S{Sq}x{Skv} c{causal}")
+
+
 @pytest.mark.parametrize("scale", [0.0, -0.125, 0.37])
 def test_scale_values(scale):
     """scale is used literally: 0 (uniform attention) and negative values are legal."""
