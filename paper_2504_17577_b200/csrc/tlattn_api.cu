@@ -98,18 +98,63 @@ int validate(const void* q, const void* k, const void* v, const void* o, const f
   return TL_OK;
 }
 
-bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
-                 int Bn, int S, int H, int D, unsigned box_rows = 128) {
-  const cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)Bn};
-  const cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2,
-                                 (cuuint64_t)S * H * D * 2};
-  const cuuint32_t box[4] = {64, 1, box_rows, 1};
+// Per-thread cache of encoded tensor maps (host-side only: a CUtensorMap is a 128-byte
+// descriptor of (address, dims, strides, box); re-encoding costs host time on every call).
+// Keyed by everything that goes into the descriptor.
+struct TmapKey {
+  const void* ptr;
+  int dtype;
+  cuuint64_t dims[4];
+  cuuint32_t box[4];
+  bool operator==(const TmapKey& o) const {
+    return ptr == o.ptr && dtype == o.dtype && std::memcmp(dims, o.dims, sizeof dims) == 0 &&
+           std::memcmp(box, o.box, sizeof box) == 0;
+  }
+};
+struct TmapCache {
+  static constexpr int N = 32;
+  TmapKey key[N];
+  CUtensorMap map[N];
+  bool used[N] = {};
+  int next = 0;
+};
+thread_local TmapCache g_tmaps;
+
+// Rank-4 map over a contiguous 16-bit tensor, dims innermost first, SWIZZLE_128B box.
+bool encode_4d_cached(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr,
+                      int dtype, const cuuint64_t (&dims)[4], const cuuint32_t (&box)[4]) {
+  TmapKey k;
+  std::memset(&k, 0, sizeof k);
+  k.ptr = ptr;
+  k.dtype = dtype;
+  std::memcpy(k.dims, dims, sizeof k.dims);
+  std::memcpy(k.box, box, sizeof k.box);
+  TmapCache& c = g_tmaps;
+  for (int i = 0; i < TmapCache::N; ++i)
+    if (c.used[i] && c.key[i] == k) {
+      *m = c.map[i];
+      return true;
+    }
+  const cuuint64_t strides[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  const int i = c.next;
+  c.next = (c.next + 1) % TmapCache::N;
+  c.key[i] = k;
+  c.map[i] = *m;
+  c.used[i] = true;
+  return true;
+}
+
+bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
+                 int Bn, int S, int H, int D, unsigned box_rows = 128) {
+  return encode_4d_cached(enc, m, ptr, dtype,
+                          {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)Bn},
+                          {64, 1, box_rows, 1});
 }
 
 template <bool BF16>
@@ -339,15 +384,8 @@ namespace {
 bool encode_2d(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
                int inner, int outer, unsigned box_inner, unsigned box_outer) {
   // rank-4 map with two unit dimensions so the kernel shares the 4-D TMA instructions
-  const cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, 1, 1};
-  const cuuint64_t row = (cuuint64_t)inner * 2;
-  const cuuint64_t strides[3] = {row, row * (cuuint64_t)outer, row * (cuuint64_t)outer};
-  const cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  return enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-             4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return encode_4d_cached(enc, m, ptr, dtype, {(cuuint64_t)inner, (cuuint64_t)outer, 1, 1},
+                          {box_inner, box_outer, 1, 1});
 }
 
 template <bool BF16>
@@ -449,12 +487,7 @@ MlaPlan plan_mla(int B, int H, int Hkv, int dev, int sm_count) {
 
 bool encode_4d(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const void* ptr, int dtype,
                const cuuint64_t (&dims)[4], const cuuint32_t (&box)[4]) {
-  const cuuint64_t strides[3] = {dims[0] * 2, dims[0] * dims[1] * 2, dims[0] * dims[1] * dims[2] * 2};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  return enc(m, dtype == TL_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-             4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return encode_4d_cached(enc, m, ptr, dtype, dims, box);
 }
 
 std::mutex g_mla_mu;

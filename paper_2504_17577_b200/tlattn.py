@@ -89,8 +89,13 @@ def _ptr(t):
     return t.data_ptr()
 
 
-def _stream_handle(stream):
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream_handle(stream, device_index=None):
     if stream is None:
+        if _raw_stream is not None and device_index is not None:
+            return _raw_stream(device_index)  # no Stream object per call (host overhead)
         return torch.cuda.current_stream().cuda_stream
     if isinstance(stream, int):
         return stream
@@ -107,10 +112,11 @@ def dtype_code(dt: torch.dtype) -> int:
 
 def tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, stream=None):
     """Direct mirror of the C entry point (device pointers or tensors)."""
+    dev = q.get_device() if isinstance(q, torch.Tensor) else None
     _check(load_library().tl_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
                                       int(B), int(Hq), int(Hkv), int(Sq), int(Skv), int(D),
                                       int(causal), float(scale), int(dtype),
-                                      _stream_handle(stream) if not isinstance(stream, int) else stream))
+                                      _stream_handle(stream, dev)))
 
 
 def tl_attn_host_workspace_bytes(B, Hq, Hkv, Sq, Skv, D, with_lse=True) -> int:

@@ -128,6 +128,31 @@ def test_mla_hard_attention_gather_bitwise():
     np.testing.assert_allclose(lse.cpu().numpy(), 4096 * scale, atol=1e-3)
 
 
+def test_mla_cuda_graph_capture():
+    # three launches, caller-provided workspace, no allocation or sync: graph-capturable
+    from paper_2504_17577_b200 import tl_mla_decode_workspace_bytes
+    B, H, Skv = 4, 128, 1000
+    q, qp, kv, kp = gen_mla(B, H, 1, Skv, DL, DR, BF, 12, "cuda")
+    sl = torch.as_tensor(gen_seqlens(B, Skv, 2), device="cuda")
+    ws = torch.empty(tl_mla_decode_workspace_bytes(B, H, 1), dtype=torch.uint8, device="cuda")
+    o = torch.empty((B, H, DL), dtype=BF, device="cuda")
+    lse = torch.empty((B, H), dtype=torch.float32, device="cuda")
+    ref_o, ref_l = mla_decode(q, qp, kv, kp, seqlens=sl)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        mla_decode(q, qp, kv, kp, seqlens=sl, out=o, lse_out=lse, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mla_decode(q, qp, kv, kp, seqlens=sl, out=o, lse_out=lse, workspace=ws)
+    o.zero_()
+    lse.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref_o) and torch.equal(lse, ref_l)
+
+
 @pytest.mark.parametrize("name", [c.name for c in MLA_CONFIGS])
 def test_mla_configs_sampled(name):
     # full-size configs in the bench's launch configuration, sampled batches

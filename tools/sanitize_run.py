@@ -1,5 +1,6 @@
 """Small forward passes for compute-sanitizer (memcheck / racecheck / synccheck):
-both kernels (CTA pair at D=128, single CTA at D=64), causal and ragged shapes."""
+both attention kernels (CTA pair at D=128, single CTA at D=64), causal and ragged shapes,
+the short-sequence pair mode, and MLA decode (32- and 64-head tiles, split + merge)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -14,3 +15,19 @@ for (B, Hq, Hkv, Sq, Skv, D, dt, causal) in [(1, 2, 1, 300, 300, 128, torch.bflo
     o, l = attention(q, k, v, causal=causal)
     torch.cuda.synchronize()
     print(B, Hq, Hkv, Sq, Skv, D, causal, float(o.float().abs().sum()), bool(torch.isfinite(l[l > -1e30]).all()))
+
+os.environ["TLATTN_UNIT_TILES"] = "1"
+q, k, v = gen_qkv(1, 2, 1, 300, 300, 128, torch.bfloat16, 6, "cuda")
+o, l = attention(q, k, v, causal=True)
+torch.cuda.synchronize()
+print("unit_tiles=1", float(o.float().abs().sum()))
+del os.environ["TLATTN_UNIT_TILES"]
+
+from paper_2504_17577_b200 import mla_decode  # noqa: E402
+from paper_2504_17577_b200.inputs import gen_mla  # noqa: E402
+for (B, H, Skv) in [(2, 32, 700), (2, 128, 700)]:
+    qm, qp, kv, kp = gen_mla(B, H, 1, Skv, 512, 64, torch.bfloat16, 9, "cuda")
+    sl = torch.tensor([700, 333], dtype=torch.int32, device="cuda")
+    om, lm = mla_decode(qm, qp, kv, kp, seqlens=sl)
+    torch.cuda.synchronize()
+    print("mla", B, H, Skv, float(om.float().abs().sum()), bool(torch.isfinite(lm).all()))
