@@ -52,7 +52,6 @@ constexpr int BLK = 128;            // keys per block (tcgen05 M of S^T)
 constexpr int NKCH = DL / 64 + 1;   // Khat chunks per block: 8 of KV + 1 of K_pe
 constexpr int NPAIRS_PER_BLK = DL / 128;  // 4 pair slots per block: KV dims [128m, 128m+128)
 constexpr int SLOT = 16384;         // one [128 keys x 64] 16-bit SWIZZLE_128B box
-constexpr int THREADS = 256;
 constexpr float RESCALE_LOG2 = 8.0f;  // conditional rescale threshold (as the attention kernel)
 constexpr int HC_MAX = 64;
 
@@ -66,7 +65,8 @@ constexpr int HC_MAX = 64;
 template <int HC>
 struct Cfg {
   static_assert(HC == 32 || HC == 64, "head tile");
-  static constexpr int R = HC / 32;                  // heads per lane after the butterfly
+  static constexpr int NSW = HC / 32;                // softmax warpgroups (32 heads each)
+  static constexpr int THREADS = 128 + 128 * NSW;    // producer, MMA, 2 spare warps + softmax
   static constexpr bool PREFETCH = HC == 32;
   static constexpr int NPAIR = PREFETCH ? 5 : 4;
   static constexpr int QCH = HC * 128;               // one [HC heads x 64] SW128 chunk of Qhat
@@ -81,7 +81,9 @@ struct Cfg {
   static constexpr int OFF_Q = OFF_PE + SLOT;
   static constexpr int OFF_P = PREFETCH ? OFF_Q + NKCH * QCH : OFF_PE;
   static constexpr int OFF_RED = OFF_Q + NKCH * QCH + (PREFETCH ? PBYTES : 0);
-  static constexpr int OFF_BAR = OFF_RED + 3 * 4 * HC * 4;  // red[2][4][HC] + redl[4][HC]
+  // per softmax group: red[2][4][32] + redl[4][32] floats, then mbc[2][2][32] floats
+  static constexpr int OFF_MBC = OFF_RED + NSW * 3 * 4 * 32 * 4;
+  static constexpr int OFF_BAR = OFF_MBC + NSW * 2 * 2 * 32 * 4;
   // pair_full/empty[NPAIR], pe_full, pe_empty, q_full, q_empty, s_full[2], s_free[2], p_full,
   // o_done, o_free
   static constexpr int NUM_BARS = 2 * NPAIR + 2 + 9;
@@ -216,20 +218,10 @@ __device__ __forceinline__ void col_reduce(const float (&in)[HC], float (&v)[HC 
   }
 }
 
-// value of per-head quantity x (lane l holds heads l*R .. l*R+R-1 in x[0..R-1]) for head h
-template <int R>
-__device__ __forceinline__ float head_val(const float (&x)[R], int h) {
-  float r = x[0];
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if ((h % R) == i) r = __shfl_sync(0xffffffffu, x[i], h / R);
-  return r;
-}
-
 template <int HC, bool BF16>
-__global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_constant__ MlaParams p) {
+__global__ void __launch_bounds__(Cfg<HC>::THREADS, 1)
+tl_mla_decode_kernel(const __grid_constant__ MlaParams p) {
   using C = Cfg<HC>;
-  constexpr int R = C::R;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
@@ -238,8 +230,8 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
   const uint32_t sPe = base + C::OFF_PE;
   const uint32_t sQ = base + C::OFF_Q;
   const uint32_t sP = base + C::OFF_P;
-  float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2][4][HC]
-  float* redl = red + 2 * 4 * HC;                             // [4][HC]
+  float* red_all = reinterpret_cast<float*>(smem + C::OFF_RED);
+  float* mbc_all = reinterpret_cast<float*>(smem + C::OFF_MBC);
   const uint32_t bar0 = base + C::OFF_BAR;
   auto bar_pair_full = [&](int s) { return bar0 + 8u * s; };
   auto bar_pair_empty = [&](int s) { return bar0 + 8u * (C::NPAIR + s); };
@@ -283,11 +275,11 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     mbar_init(bar_q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_s_full(i), 1);
-      mbar_init(bar_s_free(i), 4);
+      mbar_init(bar_s_free(i), 4 * C::NSW);  // every softmax warp
     }
-    mbar_init(bar_p_full, 4);
+    mbar_init(bar_p_full, 4 * C::NSW);
     mbar_init(bar_o_done, 1);
-    mbar_init(bar_o_free, 4);
+    mbar_init(bar_o_free, 4 * C::NSW);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_ptr_smem));
@@ -477,9 +469,19 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     __syncwarp();
   } else if (warp >= 4) {
     // ============================ softmax + epilogue ============================
+    // Warpgroup sw (of HC/32) owns heads [32 sw, 32 sw + 32) of the tile: S^T columns, its
+    // 16-B units of the P^T rows, O^T columns. One thread per key row (TMEM lane).
+    const int sw = (warp - 4) >> 2;
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;  // key within the block == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t col_s = C::TM_S + 32 * sw;   // + sb * HC
+    const uint32_t col_o = C::TM_O + 32 * sw;   // + mm * HC
+    const int hs = 32 * sw;                      // first head of this warpgroup in the tile
+    const uint32_t bar_id = 1 + sw;
+    float* red = red_all + sw * (3 * 4 * 32);    // red[2][4][32] + redl[4][32] of this group
+    float* redl = red + 2 * 4 * 32;
+    float* mbc = mbc_all + sw * (2 * 2 * 32);    // [2 buffers][m_use | alpha][32 heads]
     const float c = p.c_log2;
     const unsigned FULL = 0xffffffffu;
     uint32_t gb = 0;
@@ -487,23 +489,18 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
     SegIter si(p, part);
     Seg sg;
     while (si.next(p, sg)) {
-      float m[R];          // running max (log2 units) of heads lane*R + i (same in all 4 warps)
-      float lpart[HC];     // this key-thread's share of l for every head
+      float m = -INFINITY;  // running max (log2 units) of head hs + lane (same in all 4 warps)
+      float lpart[32];      // this key-thread's share of l for each of the group's heads
 #pragma unroll
-      for (int i = 0; i < R; ++i) m[i] = -INFINITY;
-#pragma unroll
-      for (int h = 0; h < HC; ++h) lpart[h] = 0.f;
+      for (int h = 0; h < 32; ++h) lpart[h] = 0.f;
 #pragma unroll 1
       for (int jj = 0; jj < sg.n; ++jj) {
         const uint32_t gs = gb + jj;
         const uint32_t sb = gs & 1;
         mbar_wait(bar_s_full(sb), (gs >> 1) & 1);
         tc_fence_after();
-        float s[HC];
-#pragma unroll
-        for (int cc = 0; cc < R; ++cc)
-          tmem_ld32(tmem_base + lane_off + C::TM_S + sb * HC + cc * 32,
-                    *reinterpret_cast<uint32_t(*)[32]>(s + cc * 32));
+        float s[32];
+        tmem_ld32(tmem_base + lane_off + col_s + sb * HC, *reinterpret_cast<uint32_t(*)[32]>(s));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -511,39 +508,48 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         // tail mask: keys >= len of this batch do not take part (TMA zero-fills beyond Skv)
         if ((sg.k0 + jj) * BLK + row >= sg.len) {
 #pragma unroll
-          for (int h = 0; h < HC; ++h) s[h] = -INFINITY;
+          for (int h = 0; h < 32; ++h) s[h] = -INFINITY;
         }
-        // per-head (column) max over the 128 keys: transposed butterfly inside the warp,
-        // then the 4 warps through smem (T.reduce_max)
-        float v[HC / 2];
-        col_reduce<HC, true>(s, v, lane);
-        float* rb = red + (gs & 1) * 4 * HC;
+        // per-head (column) max over the 128 keys: transposed butterfly inside the warp
+        // (lane l ends with head hs + l), then the 4 warps through smem (T.reduce_max)
+        float v[16];
+        col_reduce<32, true>(s, v, lane);
+        float* rb = red + (gs & 1) * 128;
+        rb[q4 * 32 + lane] = v[0];
+        named_bar_sync(bar_id, 128);
+        const float mx = fmaxf(fmaxf(rb[lane], rb[32 + lane]), fmaxf(rb[64 + lane], rb[96 + lane]));
+        const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
+        const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        const float alpha = ex2(m - m_use);  // scores_scale; 0 on the first block
+        const bool resc = __any_sync(FULL, alpha != 1.f);
+        // every thread needs m_use / alpha of all 32 heads: warp q4 == 0 publishes them
+        // (the 4 warps computed identical values) and the group reads them as broadcasts
+        float* mb = mbc + (gs & 1) * 64;
+        if (q4 == 0) {
+          mb[lane] = m_use;
+          mb[32 + lane] = alpha;
+        }
+        named_bar_sync(bar_id, 128);
+        float mu[32];
 #pragma unroll
-        for (int i = 0; i < R; ++i) rb[q4 * HC + lane * R + i] = v[i];
-        named_bar_sync(1, 128);
-        float m_new[R], m_use[R], alpha[R];
-        bool any_resc = false;
+        for (int h = 0; h < 32; h += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(mb + h);
+          mu[h] = t4.x; mu[h + 1] = t4.y; mu[h + 2] = t4.z; mu[h + 3] = t4.w;
+        }
+        if (resc) {
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const int hh = lane * R + i;
-          const float mx = fmaxf(fmaxf(rb[hh], rb[HC + hh]), fmaxf(rb[2 * HC + hh], rb[3 * HC + hh]));
-          const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
-          m_new[i] = (mxs > m[i] + RESCALE_LOG2) ? mxs : m[i];  // conditional rescale
-          m_use[i] = (m_new[i] == -INFINITY) ? 0.f : m_new[i];
-          alpha[i] = ex2(m[i] - m_use[i]);  // scores_scale; 0 on the first block
-          any_resc |= alpha[i] != 1.f;
+          for (int h = 0; h < 32; h += 4) {
+            const float4 a4 = *reinterpret_cast<const float4*>(mb + 32 + h);
+            lpart[h] *= a4.x; lpart[h + 1] *= a4.y; lpart[h + 2] *= a4.z; lpart[h + 3] *= a4.w;
+          }
         }
         // p = exp2(s c - m_head), l partial sums from the unrounded p (R8)
-        uint32_t pk[HC / 2];
-        const bool resc = __any_sync(FULL, any_resc);
+        uint32_t pk[16];
 #pragma unroll
-        for (int h = 0; h < HC; h += 2) {
-          const float p0 = ex2(fmaf(s[h], c, -head_val<R>(m_use, h)));
-          const float p1 = ex2(fmaf(s[h + 1], c, -head_val<R>(m_use, h + 1)));
-          if (resc) {
-            lpart[h] *= head_val<R>(alpha, h);
-            lpart[h + 1] *= head_val<R>(alpha, h + 1);
-          }
+        for (int h = 0; h < 32; h += 2) {
+          const float p0 = ex2(fmaf(s[h], c, -mu[h]));
+          const float p1 = ex2(fmaf(s[h + 1], c, -mu[h + 1]));
           lpart[h] += p0;
           lpart[h + 1] += p1;
           pk[h / 2] = pack2<BF16>(p0, p1);  // P rounded RN to the dtype (S_shared)
@@ -553,102 +559,82 @@ __global__ void __launch_bounds__(THREADS, 1) tl_mla_decode_kernel(const __grid_
         if (resc && jj > 0) {
           // acc_o *= scores_scale: O^T columns are heads
           tc_fence_after();
-          float al[HC];
-#pragma unroll
-          for (int h = 0; h < HC; ++h) al[h] = head_val<R>(alpha, h);
 #pragma unroll 1
           for (int mm = 0; mm < DL / 128; ++mm) {
+            uint32_t ov[32];
+            const uint32_t ta = tmem_base + lane_off + col_o + mm * HC;
+            tmem_ld32(ta, ov);
+            tmem_ld_wait();
 #pragma unroll
-            for (int cc = 0; cc < R; ++cc) {
-              uint32_t ov[32];
-              const uint32_t ta = tmem_base + lane_off + C::TM_O + mm * HC + cc * 32;
-              tmem_ld32(ta, ov);
-              tmem_ld_wait();
-#pragma unroll
-              for (int h = 0; h < 32; ++h)
-                ov[h] = __float_as_uint(__uint_as_float(ov[h]) * al[cc * 32 + h]);
-              tmem_st32(ta, ov);
-            }
+            for (int h = 0; h < 32; ++h) ov[h] = __float_as_uint(__uint_as_float(ov[h]) * mb[32 + h]);
+            tmem_st32(ta, ov);
           }
           tmem_st_wait();
         }
-        // P^T row (this key, HC heads) -> smem, MN-major: HC = 32 SWIZZLE_64B (16-B unit u of
-        // row r at u ^ ((r >> 1) & 3)), HC = 64 SWIZZLE_128B (unit u at u ^ (r & 7))
+        // P^T row (this key) -> smem, MN-major: HC = 32 SWIZZLE_64B (16-B unit u of row r at
+        // u ^ ((r >> 1) & 3)), HC = 64 SWIZZLE_128B (unit u at u ^ (r & 7)); this group
+        // writes units [4 sw, 4 sw + 4)
         const uint32_t prow = sP + row * C::P_ROW;
 #pragma unroll
-        for (int u = 0; u < HC / 8; ++u) {
+        for (int u0 = 0; u0 < 4; ++u0) {
+          const int u = 4 * sw + u0;
           const uint32_t pu = HC == 32 ? (u ^ ((row >> 1) & 3)) : (u ^ (row & 7));
-          st_shared_v4(prow + (pu << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          st_shared_v4(prow + (pu << 4), pk[4 * u0], pk[4 * u0 + 1], pk[4 * u0 + 2], pk[4 * u0 + 3]);
         }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_full);
-#pragma unroll
-        for (int i = 0; i < R; ++i) m[i] = m_new[i];
+        m = m_new;
       }
       // ---- epilogue: l = sum of the partial sums, O = O^T / l, LSE
       const uint32_t glast = gb + sg.n - 1;
       mbar_wait(bar_o_done, glast & 1);
       tc_fence_after();
       {
-        float v[HC / 2];
-        col_reduce<HC, false>(lpart, v, lane);
-#pragma unroll
-        for (int i = 0; i < R; ++i) redl[q4 * HC + lane * R + i] = v[i];
+        float v[16];
+        col_reduce<32, false>(lpart, v, lane);
+        redl[q4 * 32 + lane] = v[0];
       }
-      named_bar_sync(1, 128);
-      float inv[R], lse2[R];
+      named_bar_sync(bar_id, 128);
+      const float L = (redl[lane] + redl[32 + lane]) + (redl[64 + lane] + redl[96 + lane]);
+      const float m_fin = (m == -INFINITY) ? 0.f : m;
+      const float inv = (L > 0.f) ? 1.f / L : 0.f;
+      const float lse2 = (L > 0.f) ? m_fin + __log2f(L) : -INFINITY;
+      float iv[32];
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int hh = lane * R + i;
-        const float L = (redl[hh] + redl[HC + hh]) + (redl[2 * HC + hh] + redl[3 * HC + hh]);
-        const float m_fin = (m[i] == -INFINITY) ? 0.f : m[i];
-        inv[i] = (L > 0.f) ? 1.f / L : 0.f;
-        lse2[i] = (L > 0.f) ? m_fin + __log2f(L) : -INFINITY;
-      }
-      float iv[HC];
-#pragma unroll
-      for (int h = 0; h < HC; ++h) iv[h] = head_val<R>(inv, h);
+      for (int h = 0; h < 32; ++h) iv[h] = __shfl_sync(FULL, inv, h);
       const size_t wslot = ((size_t)(hgi * p.P + part) * 2 + sg.slot);
 #pragma unroll 1
       for (int mm = 0; mm < DL / 128; ++mm) {
         const int dv = mm * 128 + row;
+        uint32_t ov[32];
+        tmem_ld32(tmem_base + lane_off + col_o + mm * HC, ov);
+        tmem_ld_wait();
+        if (!sg.partial) {
+          using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
+          T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)sg.b * p.H + h0 + hs) * DL + dv;
 #pragma unroll
-        for (int cc = 0; cc < R; ++cc) {
-          uint32_t ov[32];
-          tmem_ld32(tmem_base + lane_off + C::TM_O + mm * HC + cc * 32, ov);
-          tmem_ld_wait();
-          if (!sg.partial) {
-            using T16 = typename std::conditional<BF16, __nv_bfloat16, __half>::type;
-            T16* ob = reinterpret_cast<T16*>(p.o) + ((size_t)sg.b * p.H + h0) * DL + dv;
-#pragma unroll
-            for (int h = 0; h < 32; ++h) {
-              const int hh = cc * 32 + h;
-              if (hh < nvalid) {
-                const float x = __uint_as_float(ov[h]) * iv[hh];
-                if constexpr (BF16) ob[(size_t)hh * DL] = __float2bfloat16_rn(x);
-                else ob[(size_t)hh * DL] = __float2half_rn(x);
-              }
+          for (int h = 0; h < 32; ++h) {
+            if (hs + h < nvalid) {
+              const float x = __uint_as_float(ov[h]) * iv[h];
+              if constexpr (BF16) ob[(size_t)h * DL] = __float2bfloat16_rn(x);
+              else ob[(size_t)h * DL] = __float2half_rn(x);
             }
-          } else {
-            float* wo = p.ws_o + wslot * HC * DL + dv;
-#pragma unroll
-            for (int h = 0; h < 32; ++h)
-              wo[(size_t)(cc * 32 + h) * DL] = __uint_as_float(ov[h]) * iv[cc * 32 + h];
           }
+        } else {
+          float* wo = p.ws_o + (wslot * HC + hs) * DL + dv;
+#pragma unroll
+          for (int h = 0; h < 32; ++h) wo[(size_t)h * DL] = __uint_as_float(ov[h]) * iv[h];
         }
       }
       if (q4 == 0) {
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const int hh = lane * R + i;
-          if (!sg.partial) {
-            if (p.lse != nullptr && hh < nvalid)
-              p.lse[(size_t)sg.b * p.H + h0 + hh] = lse2[i] * 0.69314718055994531f;
-          } else {
-            p.ws_lse[wslot * HC + hh] = lse2[i];
-          }
+        const int hh = hs + lane;
+        if (!sg.partial) {
+          if (p.lse != nullptr && hh < nvalid)
+            p.lse[(size_t)sg.b * p.H + h0 + hh] = lse2 * 0.69314718055994531f;
+        } else {
+          p.ws_lse[wslot * HC + hh] = lse2;
         }
       }
       tc_fence_before();

@@ -520,7 +520,7 @@ int mla_max_clusters(int dev, int cl, int sm_count) {
   if (mla_smem_attr(dev)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl * (sm_count / cl), 1, 1);
-    cfg.blockDim = dim3(mla::THREADS, 1, 1);
+    cfg.blockDim = dim3(mla::Cfg<64>::THREADS, 1, 1);
     cfg.dynamicSmemBytes = mla::Cfg<64>::SMEM_BYTES;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -550,7 +550,7 @@ int launch_mla(const mla::MlaParams& prm, int dev, int B, const int* seqlens, in
   if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prm.Hkv * prm.T * prm.P, 1, 1);
-  cfg.blockDim = dim3(mla::THREADS, 1, 1);
+  cfg.blockDim = dim3(mla::Cfg<HC>::THREADS, 1, 1);
   cfg.dynamicSmemBytes = mla::Cfg<HC>::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
