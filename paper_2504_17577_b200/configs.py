@@ -79,6 +79,11 @@ CONFIGS = {
                      "north_star target: D=128 non-causal S=8192 (C3 inputs, causal off)"),
 }
 
+# D=64 non-causal companion of C4 (A/B timing of the D=64 kernel only; not a BASELINE config)
+EXTRA = {
+    "D64N": AttnConfig("D64N", 2, 32, 32, 8192, 8192, 64, torch.float16, False, 1020, "D=64 non-causal"),
+}
+
 # The paper's own FlashAttention shapes (Table 3: batch 1, 32 heads (R13),
 # head dim 128, S in {512, 1024, 4096}); context set, SURVEY §8(d). dtype bf16 (R14).
 PAPER_T3 = {

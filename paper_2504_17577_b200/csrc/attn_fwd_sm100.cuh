@@ -79,12 +79,19 @@ template <int D>
 struct KCfg {
   static constexpr int Q_TILE_BYTES = BM * D * 2;
   static constexpr int KV_BYTES = BN * D * 2;
+  // D = 64: P lives in TMEM (columns 384..511, after S0 S1 O0 O1) and PV reads it as the
+  // TMEM A operand ("TS" MMA), so no P in SMEM and a deeper K/V ring.
+#ifndef TLATTN_P_SMEM64  // A/B experiments: keep P in SMEM at D = 64
+  static constexpr bool P_TMEM = (D == 64);
+#else
+  static constexpr bool P_TMEM = false;
+#endif
 #ifdef TLATTN_NST_OVERRIDE  // experiments only (P smem dropped)
   static constexpr int NST = TLATTN_NST_OVERRIDE;
   static constexpr int P_TILE_BYTES = 0;
 #else
-  static constexpr int NST = (D == 128) ? 3 : 6;
-  static constexpr int P_TILE_BYTES = BM * BN * 2;
+  static constexpr int NST = (D == 128) ? 3 : (P_TMEM ? 10 : 6);
+  static constexpr int P_TILE_BYTES = P_TMEM ? 0 : BM * BN * 2;
 #endif
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + TILES * Q_TILE_BYTES;
@@ -99,6 +106,7 @@ struct KCfg {
   static constexpr int SMEM_BYTES = SMEM_USED + 1024;  // slack for 1024-B alignment
   static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
   static constexpr uint32_t TMEM_O = 2 * BN;  // O0 column base
+  static constexpr uint32_t TMEM_P = 2 * BN + 2 * D;  // P0 column base (P_TMEM): BN/2 columns per tile
 };
 
 template <bool BF16>
@@ -441,6 +449,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
       const uint32_t tm_o = tmem_base + C::TMEM_O + t * D;
       const uint32_t qa = sQ + t * C::Q_TILE_BYTES;
       const uint32_t pa = sP + t * C::P_TILE_BYTES;
+      const uint32_t tm_p = tmem_base + C::TMEM_P + t * (BN / 2);
       int unit = blockIdx.x;
       int it = 0;        // K/V ring position (same sequence as the producer)
       uint32_t cs = 0;   // S MMAs issued by this tile (cumulative: barrier phases)
@@ -497,11 +506,17 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
 #ifdef TLATTN_SKIP_PV
             break;
 #endif
-            // A = P (K-major SW128, 2 x 16 KB key chunks); B = V MN-major SW128:
-            // 16 keys = 16 rows of 128 B (+2 KB); LBO = 16 KB to the next 64-wide D chunk
-            const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+            // B = V MN-major SW128: 16 keys = 16 rows of 128 B (+2 KB); LBO = 16 KB to the
+            // next 64-wide D chunk
             const uint64_t bd = make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024);
-            mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (C::P_TMEM) {
+              // A = P_t in TMEM: 16 keys = 8 columns of packed 16-bit pairs
+              mma_f16_ts(tm_o, tm_p + kk * 8, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+            } else {
+              // A = P (K-major SW128, 2 x 16 KB key chunks)
+              const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+              mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           mma_commit(bar_o_done(t));
           mma_commit(bar_kv_empty(vslot(j)));  // this tile is done with V_j
@@ -547,6 +562,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
     const uint32_t tm_s = tmem_base + lane_off + t * BN;
     const uint32_t tm_o = tmem_base + lane_off + C::TMEM_O + t * D;
     const uint32_t p_row = sP + t * C::P_TILE_BYTES + lr * 128;
+    const uint32_t tm_p_row = tmem_base + lane_off + C::TMEM_P + t * (BN / 2);
     const float c = p.c_log2;
     int unit = blockIdx.x;
     uint32_t g = 0;  // blocks processed by this tile's warpgroup (cumulative, barrier phases)
@@ -599,6 +615,13 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
             tmem_st_wait();
           }
         }
+        if constexpr (C::P_TMEM) {
+          // P row -> TMEM (this thread's lane, 64 columns of packed 16-bit pairs): the TS
+          // MMA's A operand; no SMEM traffic, no proxy fence
+          tmem_st32(tm_p_row, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+          tmem_st32(tm_p_row + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
+          tmem_st_wait();
+        } else {
         // P row -> smem, K-major SWIZZLE_128B: 16-B unit u of a 64-key chunk -> u ^ (row & 7)
 #pragma unroll
         for (int ch = 0; ch < BN / 64; ++ch) {
@@ -613,6 +636,7 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
           }
         }
         fence_proxy_async_smem();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_p_full(t));

@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2504_17577_b200 import attention  # noqa: E402
-from paper_2504_17577_b200.configs import CONFIGS  # noqa: E402
+from paper_2504_17577_b200.configs import CONFIGS, EXTRA, PAPER_T3  # noqa: E402
+CONFIGS = {**CONFIGS, **EXTRA, **PAPER_T3}
 from paper_2504_17577_b200.inputs import gen_qkv  # noqa: E402
 
 
