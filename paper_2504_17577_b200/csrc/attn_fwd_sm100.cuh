@@ -244,15 +244,11 @@ __device__ __forceinline__ void exp_row(float* s, float c, float m_use, uint32_t
   sum1 = a1 + b1;
 }
 
-// One K/V block of the online softmax for the row this thread owns (PAPER.md Fig. 18
-// P:L660-679): mask (diagonal / tail blocks only), row max, conditional running-max
-// update, p = exp2(s*c - m) with part of the exp2s on the FMA pipe, fp32 row sum of the
-// unrounded p, and P packed (RN) to the input dtype. sr[] holds the raw fp32 S row.
-template <bool BF16, int EMU>
-__device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, int limit, float c,
-                                                  float m, float& m_new_out, float& alpha_out,
-                                                  float& sum_out, uint32_t (&pk)[BN / 2]) {
-  float* s = reinterpret_cast<float*>(sr);
+// Mask (diagonal / tail blocks only), row max (T.reduce_max: in-thread, each
+// thread owns one whole S row) and the conditional running-max update of one K/V block.
+// Returns whether the block was masked; m_use is the max the exps subtract (-inf guard).
+__device__ __forceinline__ bool row_max_update(float* s, int k0, int limit, float c, float m,
+                                               float& m_new_out, float& alpha_out, float& m_use_out) {
   // any column beyond this row's last key? (diagonal / tail blocks only)
   const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
   if (masked) {
@@ -260,7 +256,6 @@ __device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, in
     for (int cc = 0; cc < BN; ++cc)
       if (k0 + cc > limit) s[cc] = -INFINITY;
   }
-  // row max (T.reduce_max): in-thread, each thread owns one whole S row
   float mq[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) mq[r] = fmax3(s[r * 32], s[r * 32 + 1], s[r * 32 + 2]);
@@ -276,6 +271,21 @@ __device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, in
   const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
   alpha_out = ex2(m - m_use);                              // scores_scale
   m_new_out = m_new;
+  m_use_out = m_use;
+  return masked;
+}
+
+// One K/V block of the online softmax for the row this thread owns (PAPER.md Fig. 18
+// P:L660-679): mask, row max, conditional running-max update (row_max_update), p =
+// exp2(s*c - m) with part of the exp2s on the FMA pipe, fp32 row sum of the unrounded p,
+// and P packed (RN) to the input dtype. sr[] holds the raw fp32 S row.
+template <bool BF16, int EMU>
+__device__ __forceinline__ void softmax_row_block(uint32_t (&sr)[BN], int k0, int limit, float c,
+                                                  float m, float& m_new_out, float& alpha_out,
+                                                  float& sum_out, uint32_t (&pk)[BN / 2]) {
+  float* s = reinterpret_cast<float*>(sr);
+  float m_use;
+  const bool masked = row_max_update(s, k0, limit, c, m, m_new_out, alpha_out, m_use);
   // p = exp2(s*c - m); row sum over the unrounded fp32 p (R8).
   // c > 0 always (scale = 0 arrives as a tiny positive c, host side), so a masked
   // s = -inf gives exp2(-inf) = 0 exactly and masked blocks use the same paired loop

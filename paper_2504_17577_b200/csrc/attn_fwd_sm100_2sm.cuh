@@ -33,7 +33,7 @@ struct KCfg2 {
   static constexpr int OFF_P = OFF_KV + NST * SLOT_BYTES;
   static constexpr int OFF_SCHED = OFF_P + TILES * P_TILE_BYTES;
   static constexpr int OFF_BAR = OFF_SCHED + 32;
-  static constexpr int NUM_BARS = 2 + 2 * NST + 12;
+  static constexpr int NUM_BARS = 2 + 2 * NST + 20;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_USED = OFF_TMEMPTR + 16;
   static constexpr int SMEM_BYTES = SMEM_USED + 1024;
@@ -52,6 +52,51 @@ __device__ __forceinline__ int tile_nblocks_rows(int r0, int rows, const AttnPar
   const long long kmax = (long long)r_last + p.Skv - p.Sq;
   if (kmax < 0) return 0;
   return min(n_all, (int)(kmax / BN) + 1);
+}
+
+// P_t is written in NPIECE pieces of BN / NPIECE keys, each with its own "P written"
+// barrier, so PV_t(j)'s first K=16 steps start while the softmax still computes the rest
+// of the row. Measured on B200: 2 pieces T0 1310 -> 1405 TFLOP/s, C2
+// 1248 -> 1336; 4 pieces lose (register spills, one proxy fence per piece).
+// TLATTN_PSPLIT=1 (experiments only) restores the single P write.
+#ifndef TLATTN_PSPLIT
+#define TLATTN_PSPLIT 2
+#endif
+constexpr int NPIECE = TLATTN_PSPLIT;
+constexpr bool P_SPLIT = NPIECE > 1;
+static_assert(NPIECE == 1 || NPIECE == 2 || NPIECE == 4, "P pieces: 1, 2 or 4");
+
+// p = exp2(s*c - m) for columns [C0, C0+64) of the row (MUFU), packed RN into pk[0..31],
+// fp32 row sums accumulated into acc (paired FADD2)
+template <bool BF16, int C0, int NC, int EMU>
+__device__ __forceinline__ void exp_cols(const float* s, float c, float m_use, uint32_t (&pk)[NC / 2],
+                                         uint64_t (&acc)[4]) {
+  const uint64_t c2 = f2pack(c, c);
+  const uint64_t nm2 = f2pack(-m_use, -m_use);
+#pragma unroll
+  for (int h = 0; h < NC; h += 32) {
+    float x[32];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint64_t x2 = ffma2(f2pack(s[C0 + h + 2 * q], s[C0 + h + 2 * q + 1]), c2, nm2);
+      f2unpack(x2, x[2 * q], x[2 * q + 1]);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (emu_pair<EMU>((C0 + h) / 2 + q)) {
+        const Exp2Poly poly;
+        poly(f2pack(x[2 * q], x[2 * q + 1]), x[2 * q], x[2 * q + 1]);
+      } else {
+        x[2 * q] = ex2(x[2 * q]);
+        x[2 * q + 1] = ex2(x[2 * q + 1]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      acc[q & 3] = fadd2(acc[q & 3], f2pack(x[2 * q], x[2 * q + 1]));
+      pk[h / 2 + q] = pack2<BF16>(x[2 * q], x[2 * q + 1]);
+    }
+  }
 }
 
 struct Unit2 {
@@ -101,6 +146,8 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
   auto bar_o_done = [&](int t) { return bar0 + 8u * (8 + 2 * C::NST + t); };
   auto bar_sched_full = [&](int i) { return bar0 + 8u * (10 + 2 * C::NST + i); };
   auto bar_sched_empty = [&](int i) { return bar0 + 8u * (12 + 2 * C::NST + i); };
+  // P_SPLIT: "piece i of P_t written" (piece 0 uses bar_p_full)
+  auto bar_p_piece = [&](int t, int i) { return i == 0 ? bar_p_full(t) : bar0 + 8u * (13 + 2 * C::NST + 3 * t + i); };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem + C::OFF_TMEMPTR);
 
   const int warp = threadIdx.x >> 5;
@@ -120,6 +167,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
       mbar_init(bar_s_full(t), 1);
       mbar_init(bar_s_free(t), 8);  // 4 softmax warps in each CTA (leader's copy is used)
       mbar_init(bar_p_full(t), 8);
+      for (int i = 1; i < 4; ++i) mbar_init(bar_p_piece(t, i), 8);
       mbar_init(bar_o_done(t), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -252,6 +300,12 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
             const uint32_t vb = sKV + sl * C::SLOT_BYTES;
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
+#ifndef TLATTN_MMA_ONLY
+              if (P_SPLIT && kk > 0 && kk % (8 / NPIECE) == 0) {  // next piece of P_t written (both CTAs)
+                mbar_wait(bar_p_piece(t, kk / (8 / NPIECE)), (cpv & 1));
+                tc_fence_after();
+              }
+#endif
               mma_f16_ss_2sm(tm_o,
                              make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024),
                              make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024), IDESC_PV,
@@ -303,6 +357,9 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
     const uint32_t p_row = sP + t * C::P_TILE_BYTES + lr * 128;
     const uint32_t lead_s_free = mapa_shared(bar_s_free(t), 0);
     const uint32_t lead_p_full = mapa_shared(bar_p_full(t), 0);
+    uint32_t lead_p_piece[NPIECE];
+#pragma unroll
+    for (int i = 0; i < NPIECE; ++i) lead_p_piece[i] = mapa_shared(bar_p_piece(t, i), 0);
     const float c = p.c_log2;
     int unit = blockIdx.x >> 1;
     uint32_t g = 0;
@@ -340,6 +397,67 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         if (lane == 0) mbar_arrive_cluster(lead_s_free);
         if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 1);
         float m_new, alpha, sum;
+        if constexpr (P_SPLIT) {
+          float* sf = reinterpret_cast<float*>(sr);
+          float m_use;
+          row_max_update(sf, j * BN, limit, c, m, m_new, alpha, m_use);
+          uint64_t acc[4];
+#pragma unroll
+          for (int a4 = 0; a4 < 4; ++a4) acc[a4] = f2pack(0.f, 0.f);
+          constexpr int NC = BN / NPIECE;
+          uint32_t pk[NC / 2];
+          exp_cols<BF16, 0, NC, 0>(sf, c, m_use, pk, acc);
+          if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 2);
+          if (j > 0) {
+            mbar_wait(bar_o_done(t), (g - 1) & 1);
+            if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 3);
+            tc_fence_after();
+            if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+              for (int cc = 0; cc < D / 32; ++cc) {
+                uint32_t ov[32];
+                tmem_ld32(tm_o + cc * 32, ov);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                tmem_st32(tm_o + cc * 32, ov);
+              }
+              tmem_st_wait();
+            }
+          }
+          if (j == 0 && g > 0) {
+            if (lr == 0) tma_store_wait_read<0>();
+            named_bar_sync(1 + t, 128);
+          }
+          auto store_piece = [&](int i) {  // P row keys [i*NC, +NC) -> K-major SW128 smem
+#pragma unroll
+            for (int v = 0; v < NC / 8; ++v) {
+              const int uu = ((i * NC) % 64) / 8 + v;  // 16-B unit within the 64-key chunk
+              const uint32_t addr = p_row + ((i * NC) / 64) * CHUNK_BYTES + ((uu ^ (lr & 7)) << 4);
+              st_shared_v4(addr, pk[v * 4], pk[v * 4 + 1], pk[v * 4 + 2], pk[v * 4 + 3]);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lead_p_piece[i]);
+          };
+          store_piece(0);
+          exp_cols<BF16, NC, NC, 0>(sf, c, m_use, pk, acc);
+          store_piece(1);
+          if constexpr (NPIECE == 4) {
+            exp_cols<BF16, 2 * NC, NC, 0>(sf, c, m_use, pk, acc);
+            store_piece(2);
+            exp_cols<BF16, 3 * NC, NC, 0>(sf, c, m_use, pk, acc);
+            store_piece(3);
+          }
+          if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 4);
+          const uint64_t t0 = fadd2(acc[0], acc[1]);
+          const uint64_t t1 = fadd2(acc[2], acc[3]);
+          float a0, a1, b0, b1;
+          f2unpack(t0, a0, a1);
+          f2unpack(t1, b0, b1);
+          sum = (a0 + b0) + (a1 + b1);
+        } else {
         uint32_t pk[BN / 2];
         softmax_row_block<BF16, TLATTN_EMU_2SM>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
         if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 2);
@@ -380,6 +498,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(lead_p_full);
         if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 4);
+        }
         l = l * alpha + sum;
         m = m_new;
       }
