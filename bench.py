@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--shard", choices=["head", "batch"], default="head")
-    ap.add_argument("--gather", action="store_true", help="also time the NCCL all-gather of O")
+    ap.add_argument("--gather", action="store_true",
+                    help="N>1: also time the replicated output: NCCL all-gather of O after the "
+                         "kernel vs the fused replicated epilogue (tl_attn_fwd_replicated)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -314,6 +316,24 @@ def run_ours(args, world, rank, local):
         b_.record()
         torch.cuda.synchronize()
         gather_ms = max_over_ranks(a.elapsed_time(b_) / 3, world)
+        # fused alternative: the kernel's epilogue stores every O tile into all
+        # ranks' full buffers (P2P over NVLink) + device flag barriers; time per call
+        # (attention + replication) next to attention + NCCL all-gather
+        from paper_2504_17577_b200.dist import ReplicatedOutput
+        rep = ReplicatedOutput(shard, cfg.B, cfg.Sq, cfg.Hq, cfg.D, cfg.dtype)
+
+        def fused():
+            rep(q, k, v, causal=cfg.causal, scale=cfg.scale)
+
+        def unfused():
+            step()
+            gather_output(o, lse, shard)
+
+        f_total, _ = time_device(fused, 5, 2, world, per_launch_events=False)
+        u_total, _ = time_device(unfused, 5, 2, world, per_launch_events=False)
+        gather_ms = {"nccl_all_gather_ms": gather_ms, "attn_plus_nccl_gather_ms": u_total / 5,
+                     "attn_fused_replicated_ms": f_total / 5}
+        rep.close()
 
     # ---- end to end through the public host-buffer entry (H2D + kernel + D2H per step)
     e2e = None

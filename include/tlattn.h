@@ -162,6 +162,67 @@ int tl_mla_decode(const void* q, const void* q_pe, const void* kv, const void* k
  * count); 0 on bad arguments or when no device is available. */
 uint64_t tl_mla_decode_workspace_bytes(int B, int H, int Hkv);
 
+/*
+ * tl_attn_fwd_replicated — tl_attn_fwd on this rank's shard with the output REPLICATED
+ * into several full-size buffers by the kernel itself (the replicated
+ * output of §8(e) fused into the epilogue; the paper lists tile-level communication
+ * primitives as future work). Each O tile leaves shared memory once per output
+ * buffer (TMA bulk-tensor stores; over NVLink when the buffer is a peer GPU's memory), so
+ * the all-gather overlaps the attention of the remaining tiles instead of following it.
+ *
+ *   q, k, v      this rank's shard, device pointers, contiguous BSHD: q [B][Sq][Hq][D],
+ *                k, v [B][Skv][Hkv][D] (as tl_attn_fwd)
+ *   o_outs       HOST array of n_outs device pointers (1 <= n_outs <= 8), each a full
+ *                output [B_total][Sq][Hq_total][D] valid in this process (own buffer, or a
+ *                peer's opened with tl_ipc_open_handle); 16-byte aligned
+ *   lse_outs     NULL, or HOST array of n_outs device pointers (entries may be NULL) to full
+ *                fp32 LSE [B_total][Hq_total][Sq]; 4-byte aligned
+ *   B_total, b_off, Hq_total, h_off
+ *                full sizes and this shard's offsets: local (b, h) is written to
+ *                (b + b_off, h + h_off); b_off + B <= B_total, h_off + Hq <= Hq_total
+ *                (head shard: b_off = 0, h_off = rank * Hq; batch shard: h_off = 0)
+ *   other arguments as tl_attn_fwd
+ *
+ * Only this shard's rows of each output are written. One kernel launch, stream-ordered, no
+ * allocation, graph-capturable. Writes into peer memory are complete when the kernel is;
+ * readers on other ranks must order after it (tl_peer_barrier). Ownership: the caller owns
+ * every buffer (and the IPC mappings). Errors as tl_attn_fwd, plus TL_ERR_INVALID_VALUE for
+ * NULL o_outs / entries, n_outs outside [1, 8] or offsets outside the full sizes.
+ */
+int tl_attn_fwd_replicated(const void* q, const void* k, const void* v,
+                           void* const* o_outs, float* const* lse_outs, int n_outs,
+                           int B_total, int b_off, int Hq_total, int h_off,
+                           int B, int Hq, int Hkv, int Sq, int Skv, int D,
+                           int causal, float scale, int dtype, void* stream);
+
+/*
+ * tl_peer_barrier — stream-ordered device-side barrier among `world` ranks (one kernel).
+ *
+ *   flags   HOST array of `world` device pointers (world <= 8): flags[r] = rank r's array
+ *           of `world` uint32 counters as mapped in THIS process (flags[rank] = own array;
+ *           peers' opened with tl_ipc_open_handle); zero-initialised once by their owners
+ *   rank    this rank; epoch: a value that increases by 1 on every use (wraps mod 2^32)
+ *
+ * Rank `rank` stores `epoch` into flags[r][rank] for every r (system-scope release, after
+ * this stream's earlier work) and waits until flags[rank][r] >= epoch for every r
+ * (acquire). After it, this stream sees every rank's writes issued before that rank's
+ * barrier (e.g. tl_attn_fwd_replicated into this rank's output). All ranks must call it
+ * with the same epoch sequence, otherwise it waits forever.
+ * Errors: TL_ERR_INVALID_VALUE (NULL / misaligned flags, bad world / rank), TL_ERR_CUDA.
+ */
+int tl_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream);
+
+/* CUDA IPC helpers for the peer buffers above (wrappers over cudaIpc*MemHandle): a handle
+ * is tl_ipc_handle_bytes() opaque bytes the caller ships to other processes (e.g. with
+ * torch.distributed.all_gather_object). tl_ipc_get_handle: dev_ptr must be the base of a
+ * cudaMalloc allocation. tl_ipc_open_handle maps another process's allocation into this
+ * one (same or peer GPU); close with tl_ipc_close_handle. Return TL_OK, TL_ERR_INVALID_VALUE
+ * (NULL arguments) or TL_ERR_CUDA. */
+int tl_ipc_handle_bytes(void);
+int tl_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int tl_ipc_open_handle(const void* handle, void** dev_ptr_out);
+int tl_ipc_close_handle(void* dev_ptr);
+
 /* Static, NUL-terminated description of a tl_status code. Never NULL. */
 const char* tl_attn_strerror(int status);
 
@@ -169,8 +230,8 @@ const char* tl_attn_strerror(int status);
 int tl_attn_version(void);
 
 /* Number of kernel launches the most recent successful tl_attn_fwd / tl_attn_fwd_host /
- * tl_gemm / tl_mla_decode call on this host thread issued (tl_attn_fwd: 1,
- * tl_mla_decode: 3). For accounting in benchmarks. */
+ * tl_attn_fwd_replicated / tl_peer_barrier / tl_gemm / tl_mla_decode call on this host
+ * thread issued (tl_attn_fwd: 1, tl_mla_decode: 3). For accounting in benchmarks. */
 int tl_attn_last_launch_count(void);
 
 #ifdef __cplusplus

@@ -27,4 +27,9 @@ from .tlattn import (  # noqa: F401
     tl_attn_last_launch_count,
     tl_attn_strerror,
     tl_attn_version,
+    tl_attn_fwd_replicated,
+    tl_peer_barrier,
+    tl_ipc_get_handle,
+    tl_ipc_open_handle,
+    tl_ipc_close_handle,
 )

@@ -52,7 +52,48 @@ struct AttnParams {
   int n_units;       // B * Hq * n_mblk
   int unit_tiles;    // CTA-pair kernel: query tiles (of 256 rows) per unit, 2 or 1 (short Sq)
   unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
+  static constexpr bool kRepl = false;
 };
+
+// Replicated output (tl_attn_fwd_replicated): the epilogue writes each O
+// tile (and LSE row) of this rank's shard straight into the full [B_total][Sq][Hq_total][D]
+// output of every rank (peer buffers mapped into this process), at batch / head offsets
+// b_off / h_off. The all-gather of O becomes part of the kernel's store stream.
+constexpr int kMaxOuts = 8;
+struct AttnParamsRepl : AttnParams {
+  CUtensorMap tm_out[kMaxOuts];  // full outputs, (D, Hq_total, Sq, B_total), box (64, 1, 128, 1)
+  void* o_out[kMaxOuts];         // the same buffers as raw pointers (row-store epilogue)
+  float* lse_out[kMaxOuts];      // full LSE [B_total][Hq_total][Sq] per output, or all NULL
+  int n_out, b_off, h_off, Hq_total;
+  static constexpr bool kRepl = true;
+};
+
+// Row-store epilogue helper: O row (16-byte pieces) and LSE of one query row to the
+// output(s); `pieces` are 16-B chunks at byte offset `off` within the D-row.
+template <class PT>
+__device__ __forceinline__ uint8_t* out_row(const PT& p, int r, int b, int h, int row, int D) {
+  if constexpr (PT::kRepl) {
+    return reinterpret_cast<uint8_t*>(p.o_out[r]) +
+           ((((size_t)(b + p.b_off) * p.Sq + row) * p.Hq_total + (h + p.h_off)) * D) * 2;
+  } else {
+    return reinterpret_cast<uint8_t*>(p.o) + ((((size_t)b * p.Sq + row) * p.Hq + h) * D) * 2;
+  }
+}
+template <class PT>
+__device__ __forceinline__ void store_lse(const PT& p, int b, int h, int row, float v) {
+  if constexpr (PT::kRepl) {
+    for (int r = 0; r < p.n_out; ++r)
+      if (p.lse_out[r] != nullptr)
+        p.lse_out[r][((size_t)(b + p.b_off) * p.Hq_total + (h + p.h_off)) * p.Sq + row] = v;
+  } else {
+    if (p.lse != nullptr) p.lse[((size_t)b * p.Hq + h) * p.Sq + row] = v;
+  }
+}
+template <class PT>
+__device__ __forceinline__ int n_outputs(const PT& p) {
+  if constexpr (PT::kRepl) return p.n_out;
+  else return 1;
+}
 
 // Debug-only pipeline trace (compile with -DTLATTN_TRACE): clock64 stamps of the first
 // unit of CTA 0 (the pair leader), used to inspect the MMA / softmax overlap.
@@ -316,9 +357,9 @@ __device__ __forceinline__ Unit decode_unit(int u, const AttnParams& p) {
   return U;
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, class PT = AttnParams>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
+tl_attn_fwd_kernel(const __grid_constant__ PT p) {
   using C = KCfg<D>;
   // K/V load order: D=128 loads K_{j+1} ahead of V_j (MMA consumption order, measured
   // faster with the 3-slot ring); D=64 has a 6-slot ring and keeps K_j, V_j pairs.
@@ -662,8 +703,6 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
       }
       const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
       const bool row_ok = row < p.Sq;
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
-                      ((((size_t)U.b * p.Sq + (row_ok ? row : 0)) * p.Hq + U.h) * D) * 2;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t ov[32];
@@ -679,16 +718,18 @@ tl_attn_fwd_kernel(const __grid_constant__ AttnParams p) {
         for (int e = 0; e < 16; ++e)
           pkd[e] = pack2<BF16>(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
         if (row_ok) {
+          for (int r = 0; r < n_outputs(p); ++r) {
+            uint8_t* orow = out_row(p, r, U.b, U.h, row, D);
 #pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4)
-            st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2],
-                         pkd[4 * v4 + 3]);
+            for (int v4 = 0; v4 < 4; ++v4)
+              st_global_v4(orow + cc * 64 + v4 * 16, pkd[4 * v4], pkd[4 * v4 + 1], pkd[4 * v4 + 2],
+                           pkd[4 * v4 + 3]);
+          }
         }
       }
-      if (p.lse != nullptr && row_ok) {
+      if (row_ok) {
         // lse = ln sum exp(scale*s) = (m + log2 l) ln 2, m in log2 units (reading R5)
-        p.lse[((size_t)U.b * p.Hq + U.h) * p.Sq + row] =
-            (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+        store_lse(p, U.b, U.h, row, (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY);
       }
       tc_fence_before();  // O_t reads complete before the next unit's first PV_t overwrites
 

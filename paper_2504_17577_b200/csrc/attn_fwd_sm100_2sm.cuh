@@ -119,9 +119,9 @@ __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
   return U;
 }
 
-template <bool BF16>
+template <bool BF16, class PT = AttnParams>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
-tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
+tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
   using C = KCfg2;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -542,15 +542,21 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ AttnParams p) {
         const int row0 = U.r0 + 256 * t + 128 * (int)rank;
         if (row0 < p.Sq) {
 #pragma unroll
-          for (int c2 = 0; c2 < D / 64; ++c2)
-            tma_store_4d(&p.tm_o, sP + t * C::P_TILE_BYTES + c2 * CHUNK_BYTES, c2 * 64, U.h, row0, U.b);
+          for (int c2 = 0; c2 < D / 64; ++c2) {
+            const uint32_t src = sP + t * C::P_TILE_BYTES + c2 * CHUNK_BYTES;
+            if constexpr (PT::kRepl) {
+              // replicated output: the same staged tile to every rank's full O (N2)
+              for (int r = 0; r < p.n_out; ++r)
+                tma_store_4d(&p.tm_out[r], src, c2 * 64, U.h + p.h_off, row0, U.b + p.b_off);
+            } else {
+              tma_store_4d(&p.tm_o, src, c2 * 64, U.h, row0, U.b);
+            }
+          }
         }
         tma_store_commit();
       }
-      if (p.lse != nullptr && row_ok) {
-        p.lse[((size_t)U.b * p.Hq + U.h) * p.Sq + row] =
-            (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-      }
+      if (row_ok)
+        store_lse(p, U.b, U.h, row, (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY);
       tc_fence_before();
       mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
       const int nxt = clc_query(sSched + 16 * (k & 1));

@@ -157,9 +157,9 @@ bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const vo
                           {64, 1, box_rows, 1});
 }
 
-template <bool BF16>
-int launch_2sm(const AttnParams& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
-  auto kern = tl_attn_fwd_kernel_2sm<BF16>;
+template <bool BF16, class PT>
+int launch_2sm(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
+  auto kern = tl_attn_fwd_kernel_2sm<BF16, PT>;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!di.smem_set[inst]) {
@@ -184,9 +184,9 @@ bool use_2sm(int D) {
   return !(e && std::strcmp(e, "1cta") == 0);
 }
 
-template <int D, bool BF16>
-int launch(const AttnParams& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
-  auto kern = tl_attn_fwd_kernel<D, BF16>;
+template <int D, bool BF16, class PT>
+int launch(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
+  auto kern = tl_attn_fwd_kernel<D, BF16, PT>;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!di.smem_set[inst]) {
@@ -203,30 +203,23 @@ int launch(const AttnParams& prm, DeviceInfo& di, int inst, cudaStream_t stream)
   return TL_OK;
 }
 
-}  // namespace
-
-extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B,
-                           int Hq, int Hkv, int Sq, int Skv, int D, int causal, float scale,
-                           int dtype, void* stream) {
-  g_last_launches = 0;
-  int rc = validate(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype);
-  if (rc != TL_OK) return rc;
+// Shared by tl_attn_fwd and tl_attn_fwd_replicated: input tensor maps, sizes, unit
+// geometry; then the launch of the kernel instantiated for the parameter type PT.
+template <class PT>
+int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq, int Hkv,
+             int Sq, int Skv, int D, int causal, float scale, int dtype, void* stream) {
   int dev;
   DeviceInfo* di;
+  int rc;
   if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
   auto enc = get_encode();
   if (!enc) return TL_ERR_CUDA;
 
   const bool pair = use_2sm(D);
-  AttnParams prm;
-  std::memset(&prm, 0, sizeof(prm));
   if (!encode_bshd(enc, &prm.tm_q, q, dtype, B, Sq, Hq, D) ||
       !encode_bshd(enc, &prm.tm_k, k, dtype, B, Skv, Hkv, D, pair ? 64u : 128u) ||
-      !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D) ||
-      !encode_bshd(enc, &prm.tm_o, o, dtype, B, Sq, Hq, D))
+      !encode_bshd(enc, &prm.tm_v, v, dtype, B, Skv, Hkv, D))
     return TL_ERR_CUDA;
-  prm.o = o;
-  prm.lse = lse;
   prm.B = B;
   prm.Hq = Hq;
   prm.Hkv = Hkv;
@@ -260,11 +253,184 @@ extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o,
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool bf = dtype == TL_DTYPE_BF16;
-  if (pair) rc = bf ? launch_2sm<true>(prm, *di, 4, st) : launch_2sm<false>(prm, *di, 5, st);
-  else if (D == 128) rc = bf ? launch<128, true>(prm, *di, 0, st) : launch<128, false>(prm, *di, 1, st);
-  else rc = bf ? launch<64, true>(prm, *di, 2, st) : launch<64, false>(prm, *di, 3, st);
+  const int i0 = PT::kRepl ? 6 : 0;  // per-instantiation "smem attribute set" slots
+  if (pair) rc = bf ? launch_2sm<true>(prm, *di, i0 + 4, st) : launch_2sm<false>(prm, *di, i0 + 5, st);
+  else if (D == 128) rc = bf ? launch<128, true>(prm, *di, i0 + 0, st) : launch<128, false>(prm, *di, i0 + 1, st);
+  else rc = bf ? launch<64, true>(prm, *di, i0 + 2, st) : launch<64, false>(prm, *di, i0 + 3, st);
   if (rc == TL_OK) g_last_launches = 1;
   return rc;
+}
+
+}  // namespace
+
+extern "C" int tl_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B,
+                           int Hq, int Hkv, int Sq, int Skv, int D, int causal, float scale,
+                           int dtype, void* stream) {
+  g_last_launches = 0;
+  int rc = validate(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype);
+  if (rc != TL_OK) return rc;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  AttnParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (!encode_bshd(enc, &prm.tm_o, o, dtype, B, Sq, Hq, D)) return TL_ERR_CUDA;
+  prm.o = o;
+  prm.lse = lse;
+  return run_attn(prm, q, k, v, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, stream);
+}
+
+extern "C" int tl_attn_fwd_replicated(const void* q, const void* k, const void* v,
+                                      void* const* o_outs, float* const* lse_outs, int n_outs,
+                                      int B_total, int b_off, int Hq_total, int h_off, int B,
+                                      int Hq, int Hkv, int Sq, int Skv, int D, int causal,
+                                      float scale, int dtype, void* stream) {
+  g_last_launches = 0;
+  if (!o_outs || n_outs < 1 || n_outs > kMaxOuts) return TL_ERR_INVALID_VALUE;
+  for (int r = 0; r < n_outs; ++r)
+    if (!o_outs[r]) return TL_ERR_INVALID_VALUE;
+  int rc = validate(q, k, v, o_outs[0], nullptr, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype);
+  if (rc != TL_OK) return rc;
+  if (b_off < 0 || h_off < 0 || B_total < 1 || Hq_total < 1 || (long long)b_off + B > B_total ||
+      (long long)h_off + Hq > Hq_total)
+    return TL_ERR_INVALID_VALUE;
+  for (int r = 0; r < n_outs; ++r) {
+    if (reinterpret_cast<uintptr_t>(o_outs[r]) % 16 != 0) return TL_ERR_UNSUPPORTED;
+    if (lse_outs && lse_outs[r] && reinterpret_cast<uintptr_t>(lse_outs[r]) % 4 != 0)
+      return TL_ERR_UNSUPPORTED;
+  }
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  AttnParamsRepl prm;
+  std::memset(&prm, 0, sizeof(prm));
+  for (int r = 0; r < n_outs; ++r) {
+    if (!encode_bshd(enc, &prm.tm_out[r], o_outs[r], dtype, B_total, Sq, Hq_total, D))
+      return TL_ERR_CUDA;
+    prm.o_out[r] = o_outs[r];
+    prm.lse_out[r] = lse_outs ? lse_outs[r] : nullptr;
+  }
+  prm.n_out = n_outs;
+  prm.b_off = b_off;
+  prm.h_off = h_off;
+  prm.Hq_total = Hq_total;
+  return run_attn(prm, q, k, v, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, stream);
+}
+
+// ------------------------------------------------------------------ peer memory (N2)
+namespace {
+struct PeerFlags {
+  uint32_t* ptr[kMaxOuts];
+};
+// One block, `world` threads: thread i publishes `epoch` into rank i's flag slot [rank]
+// (system-scope release: this rank's earlier writes into rank i's memory — the replicated
+// O / LSE of the previous kernels on this stream — are visible before the flag), then
+// waits until its own slot [i] holds >= epoch (acquire: rank i's writes are visible).
+__global__ void tl_peer_barrier_kernel_v(const PeerFlags f, int world, int rank, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i >= world) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.ptr[i] + rank), "r"(epoch) : "memory");
+  const uint32_t* mine = f.ptr[rank] + i;
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+  } while ((int32_t)(v - epoch) < 0);
+}
+}  // namespace
+
+extern "C" int tl_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+                               void* stream) {
+  g_last_launches = 0;
+  if (!flags || world < 1 || world > kMaxOuts || rank < 0 || rank >= world)
+    return TL_ERR_INVALID_VALUE;
+  PeerFlags f;
+  std::memset(&f, 0, sizeof f);
+  for (int r = 0; r < world; ++r) {
+    if (!flags[r] || reinterpret_cast<uintptr_t>(flags[r]) % 4 != 0) return TL_ERR_INVALID_VALUE;
+    f.ptr[r] = flags[r];
+  }
+  int dev;
+  DeviceInfo* di;
+  int rc;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  tl_peer_barrier_kernel_v<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(f, world, rank, epoch);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  g_last_launches = 1;
+  return TL_OK;
+}
+
+// Handle blob = cudaIpcMemHandle_t of the allocation + the byte offset of dev_ptr inside it
+// (torch's caching allocator sub-allocates, and cudaIpcOpenMemHandle maps the allocation
+// base), so the opened pointer is the same tensor in the other process.
+struct IpcBlob {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+};
+
+extern "C" int tl_ipc_handle_bytes(void) { return (int)sizeof(IpcBlob); }
+
+extern "C" int tl_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return TL_ERR_INVALID_VALUE;
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!get_range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault,
+                                           &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        return TL_ERR_CUDA;
+      get_range = reinterpret_cast<GetRange>(fn);
+    }
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return TL_ERR_CUDA;
+  IpcBlob blob;
+  std::memset(&blob, 0, sizeof blob);
+  if (cudaIpcGetMemHandle(&blob.h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  blob.offset = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+  std::memcpy(handle_out, &blob, sizeof blob);
+  return TL_OK;
+}
+
+extern "C" int tl_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return TL_ERR_INVALID_VALUE;
+  IpcBlob blob;
+  std::memcpy(&blob, handle, sizeof blob);
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, blob.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  *dev_ptr_out = static_cast<uint8_t*>(base) + blob.offset;
+  return TL_OK;
+}
+
+// dev_ptr: the pointer tl_ipc_open_handle returned (offset into the mapped allocation)
+extern "C" int tl_ipc_close_handle(void* dev_ptr) {
+  if (!dev_ptr) return TL_ERR_INVALID_VALUE;
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) !=
+          cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return TL_ERR_CUDA;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return TL_ERR_CUDA;
+  if (cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  return TL_OK;
 }
 
 // ------------------------------------------------------------------ host-buffer entry

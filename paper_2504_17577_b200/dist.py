@@ -80,3 +80,92 @@ def gather_output(o_local: torch.Tensor, lse_local: torch.Tensor | None, shard: 
         else:
             lse_full = lbuf.view(w, Bl2, Hl2, S2).permute(1, 0, 2, 3).reshape(Bl2, w * Hl2, S2)
     return o_full, lse_full
+
+
+def replica_layout(shard: Shard, B: int, Hq: int):
+    """(B_total, b_off, Hq_total, h_off) of this rank's shard inside the full output."""
+    return B, shard.b.start, Hq, shard.hq.start
+
+
+def _al(x: int, a: int = 256) -> int:
+    return (x + a - 1) // a * a
+
+
+class ReplicatedOutput:
+    """Full O[B, Sq, Hq, D] (and LSE[B, Hq, Sq]) on every rank, written by the attention
+    kernel itself (include/tlattn.h tl_attn_fwd_replicated).
+
+    Each rank owns one device allocation [O | LSE | flags], maps every peer's allocation
+    into its address space once (CUDA IPC handles exchanged with all_gather_object), and
+    on every call runs its shard with the epilogue storing each O tile into all ranks'
+    buffers (NVLink P2P stores for peer GPUs), followed by a device-side flag barrier
+    (tl_peer_barrier) so each rank's stream sees every shard. A barrier also precedes the
+    kernel (pre_barrier) so no rank overwrites a buffer a peer may still be reading.
+    world <= 8. Host logic only: every byte of O moves inside the kernels.
+    """
+
+    def __init__(self, shard: Shard, B: int, Sq: int, Hq: int, D: int, dtype, with_lse=True,
+                 device=None, group=None):
+        from . import tlattn as T
+        if shard.world > 8:
+            raise ValueError("replicated output supports up to 8 ranks")
+        self.shard, self.B, self.Sq, self.Hq, self.D = shard, B, Sq, Hq, D
+        self.dtype, self.with_lse = dtype, with_lse
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        esz = torch.empty((), dtype=dtype).element_size()
+        o_bytes = B * Sq * Hq * D * esz
+        lse_bytes = B * Hq * Sq * 4 if with_lse else 0
+        self.off_lse = _al(o_bytes)
+        self.off_flags = self.off_lse + _al(lse_bytes)
+        total = self.off_flags + _al(4 * 8)
+        self.buf = torch.zeros(total, dtype=torch.uint8, device=dev)
+        self.o = self.buf[:o_bytes].view(dtype).view(B, Sq, Hq, D)
+        self.lse = (self.buf[self.off_lse:self.off_lse + lse_bytes].view(torch.float32)
+                    .view(B, Hq, Sq) if with_lse else None)
+        torch.cuda.synchronize(dev)
+        handle = T.tl_ipc_get_handle(self.buf)
+        handles = [None] * shard.world
+        dist.all_gather_object(handles, handle, group=group)
+        self.bases, self._opened = [], []
+        for r, h in enumerate(handles):
+            if r == shard.rank:
+                self.bases.append(self.buf.data_ptr())
+            else:
+                p = T.tl_ipc_open_handle(h)
+                self._opened.append(p)
+                self.bases.append(p)
+        self.o_ptrs = list(self.bases)
+        self.lse_ptrs = [b + self.off_lse for b in self.bases] if with_lse else None
+        self.flag_ptrs = [b + self.off_flags for b in self.bases]
+        self.epoch = 0
+        self.group = group
+        dist.barrier(group=group)  # every rank's flags are zeroed and mapped before first use
+
+    def barrier(self, stream=None):
+        from . import tlattn as T
+        self.epoch += 1
+        T.tl_peer_barrier(self.flag_ptrs, self.shard.rank, self.epoch, stream)
+
+    def __call__(self, q, k, v, causal=False, scale=None, stream=None, pre_barrier=True):
+        """Run this rank's shard (local q [B_l, Sq, Hq_l, D], k/v [B_l, Skv, Hkv_l, D]) and
+        return the full (O, LSE) views of this rank's buffer, complete on `stream`."""
+        import math
+
+        from . import tlattn as T
+        Bl, Sq, Hl, D = q.shape
+        Skv, Hkvl = k.shape[1], k.shape[2]
+        scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+        B_total, b_off, Hq_total, h_off = replica_layout(self.shard, self.B, self.Hq)
+        if pre_barrier:
+            self.barrier(stream)
+        T.tl_attn_fwd_replicated(q, k, v, self.o_ptrs, self.lse_ptrs, B_total, b_off, Hq_total,
+                                 h_off, Bl, Hl, Hkvl, Sq, Skv, D, int(bool(causal)), scale,
+                                 T.dtype_code(q.dtype), stream)
+        self.barrier(stream)
+        return self.o, self.lse
+
+    def close(self):
+        from . import tlattn as T
+        for p in self._opened:
+            T.tl_ipc_close_handle(p)
+        self._opened = []

@@ -60,6 +60,20 @@ def load_library(path: str | None = None):
         lib.tl_mla_decode_workspace_bytes.restype = U64
         lib.tl_attn_last_launch_count.argtypes = []
         lib.tl_attn_last_launch_count.restype = I
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        lib.tl_attn_fwd_replicated.argtypes = [P, P, P, PP, PP, I, I, I, I, I, I, I, I, I, I, I, I,
+                                               F, I, P]
+        lib.tl_attn_fwd_replicated.restype = I
+        lib.tl_peer_barrier.argtypes = [PP, I, I, ctypes.c_uint32, P]
+        lib.tl_peer_barrier.restype = I
+        lib.tl_ipc_handle_bytes.argtypes = []
+        lib.tl_ipc_handle_bytes.restype = I
+        lib.tl_ipc_get_handle.argtypes = [P, P]
+        lib.tl_ipc_get_handle.restype = I
+        lib.tl_ipc_open_handle.argtypes = [P, PP]
+        lib.tl_ipc_open_handle.restype = I
+        lib.tl_ipc_close_handle.argtypes = [P]
+        lib.tl_ipc_close_handle.restype = I
         _lib = lib
         return lib
 
@@ -117,6 +131,49 @@ def tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, causal, scale, dtype, s
                                       int(B), int(Hq), int(Hkv), int(Sq), int(Skv), int(D),
                                       int(causal), float(scale), int(dtype),
                                       _stream_handle(stream, dev)))
+
+
+def _ptr_array(ptrs):
+    if ptrs is None:
+        return None
+    arr = (ctypes.c_void_p * len(ptrs))(*[_ptr(x) for x in ptrs])
+    return ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+
+
+def tl_attn_fwd_replicated(q, k, v, o_outs, lse_outs, B_total, b_off, Hq_total, h_off, B, Hq, Hkv,
+                           Sq, Skv, D, causal, scale, dtype, stream=None):
+    """Direct mirror of the C entry point: this rank's shard written into every output in
+    ``o_outs`` (device pointers valid in this process, e.g. IPC-mapped peer buffers)."""
+    dev = q.get_device() if isinstance(q, torch.Tensor) else None
+    oa = _ptr_array(o_outs)
+    la = _ptr_array(lse_outs)
+    _check(load_library().tl_attn_fwd_replicated(
+        _ptr(q), _ptr(k), _ptr(v), oa, la, len(o_outs), int(B_total), int(b_off), int(Hq_total),
+        int(h_off), int(B), int(Hq), int(Hkv), int(Sq), int(Skv), int(D), int(causal), float(scale),
+        int(dtype), _stream_handle(stream, dev)))
+
+
+def tl_peer_barrier(flags, rank, epoch, stream=None):
+    """Device-side barrier over the ranks whose flag arrays are ``flags`` (one per rank)."""
+    _check(load_library().tl_peer_barrier(_ptr_array(flags), len(flags), int(rank),
+                                          int(epoch) & 0xFFFFFFFF, _stream_handle(stream)))
+
+
+def tl_ipc_get_handle(t) -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(lib.tl_ipc_handle_bytes())
+    _check(lib.tl_ipc_get_handle(_ptr(t), buf))
+    return buf.raw
+
+
+def tl_ipc_open_handle(handle: bytes) -> int:
+    out = ctypes.c_void_p()
+    _check(load_library().tl_ipc_open_handle(ctypes.c_char_p(handle), ctypes.byref(out)))
+    return int(out.value)
+
+
+def tl_ipc_close_handle(ptr: int):
+    _check(load_library().tl_ipc_close_handle(ptr))
 
 
 def tl_attn_host_workspace_bytes(B, Hq, Hkv, Sq, Skv, D, with_lse=True) -> int:

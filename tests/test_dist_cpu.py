@@ -98,3 +98,25 @@ def test_sharded_forward_reassembles_bitwise(world, mode, causal):
     assert o_got.shape == o_ref.shape and lse_got.shape == lse_ref.shape
     assert np.array_equal(o_got, o_ref)
     assert np.array_equal(lse_got, lse_ref)
+
+
+@pytest.mark.parametrize("mode", ["head", "batch"])
+@pytest.mark.parametrize("w", [1, 2, 4])
+def test_replica_layout_covers_full_output_once(mode, w):
+    """The fused replicated epilogue (tl_attn_fwd_replicated) writes local (b, h) of rank r
+    to (b + b_off, h + h_off) of every output: over all ranks each (b, h) of the full
+    output is written exactly once, and each local GQA group keeps its kv heads."""
+    from paper_2504_17577_b200.dist import replica_layout
+    hits = np.zeros((B, HQ), dtype=int)
+    for r in range(w):
+        sh = make_shard(mode, r, w, B, HQ, HKV)
+        Bt, b_off, Ht, h_off = replica_layout(sh, B, HQ)
+        assert (Bt, Ht) == (B, HQ)
+        Bl, Hl, Hkvl = sh.local_dims(B, HQ, HKV)
+        assert b_off == sh.b.start and h_off == sh.hq.start
+        hits[b_off:b_off + Bl, h_off:h_off + Hl] += 1
+        # the kernel maps local query head h to local kv head h // (Hl / Hkvl); globally
+        # that must be the same kv head as h_off + h -> (h_off + h) // (HQ / HKV)
+        for h in range(Hl):
+            assert sh.hkv.start + h // (Hl // Hkvl) == (h_off + h) // (HQ // HKV)
+    assert (hits == 1).all()
