@@ -66,39 +66,6 @@ constexpr int NPIECE = TLATTN_PSPLIT;
 constexpr bool P_SPLIT = NPIECE > 1;
 static_assert(NPIECE == 1 || NPIECE == 2 || NPIECE == 4, "P pieces: 1, 2 or 4");
 
-// p = exp2(s*c - m) for columns [C0, C0+64) of the row (MUFU), packed RN into pk[0..31],
-// fp32 row sums accumulated into acc (paired FADD2)
-template <bool BF16, int C0, int NC, int EMU>
-__device__ __forceinline__ void exp_cols(const float* s, float c, float m_use, uint32_t (&pk)[NC / 2],
-                                         uint64_t (&acc)[4]) {
-  const uint64_t c2 = f2pack(c, c);
-  const uint64_t nm2 = f2pack(-m_use, -m_use);
-#pragma unroll
-  for (int h = 0; h < NC; h += 32) {
-    float x[32];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const uint64_t x2 = ffma2(f2pack(s[C0 + h + 2 * q], s[C0 + h + 2 * q + 1]), c2, nm2);
-      f2unpack(x2, x[2 * q], x[2 * q + 1]);
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      if (emu_pair<EMU>((C0 + h) / 2 + q)) {
-        const Exp2Poly poly;
-        poly(f2pack(x[2 * q], x[2 * q + 1]), x[2 * q], x[2 * q + 1]);
-      } else {
-        x[2 * q] = ex2(x[2 * q]);
-        x[2 * q + 1] = ex2(x[2 * q + 1]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      acc[q & 3] = fadd2(acc[q & 3], f2pack(x[2 * q], x[2 * q + 1]));
-      pk[h / 2 + q] = pack2<BF16>(x[2 * q], x[2 * q + 1]);
-    }
-  }
-}
-
 struct Unit2 {
   int b, h, hkv, r0, n0, n1;
   int tiles;  // query tiles this unit owns (2, or 1 in the short-sequence mode)
