@@ -240,10 +240,13 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           mbar_wait(bar_q_full, k & 1);
           auto issue_s = [&](int j) {
             const int sl = kpos(j) % C::NST;
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 0);
             mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 1);
 #ifndef TLATTN_MMA_ONLY
             if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // both CTAs read S_t
 #endif
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 2);
             tc_fence_after();
             const uint32_t kb = sKV + sl * C::SLOT_BYTES;
 #pragma unroll
@@ -259,10 +262,13 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           };
           auto issue_pv = [&](int j) {
             const int sl = vpos(j) % C::NST;
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 3);
             mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 4);
 #ifndef TLATTN_MMA_ONLY
             mbar_wait(bar_p_full(t), cpv & 1);  // P_t written in both CTAs
 #endif
+            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 5);
             tc_fence_after();
             const uint32_t vb = sKV + sl * C::SLOT_BYTES;
 #pragma unroll
