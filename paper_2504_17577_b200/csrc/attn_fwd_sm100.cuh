@@ -177,8 +177,11 @@ __device__ __forceinline__ int tile_nblocks(int r0, const AttnParams& p) {
 // otherwise keep the stale max, so p = exp2(c s - m) <= 2^8 stays well inside fp16/bf16
 // range and the result is unchanged up to rounding (O and l use the same m).
 constexpr float RESCALE_LOG2 = 8.0f;
+// The CTA is launched with 168 x 384 = 64512 registers (__launch_bounds__(384, 1)); the
+// split must fit that pool (216 for the softmax warpgroups would need 65536 and blocks
+// setmaxnreg.inc forever — measured: the watchdog traps).
 constexpr uint32_t REGS_SMALL = 88;     // warpgroup 0: 128 x 88
-constexpr uint32_t REGS_SOFTMAX = 208;  // warpgroups 1-2: 256 x 208 (total 64512 <= 64K)
+constexpr uint32_t REGS_SOFTMAX = 208;  // warpgroups 1-2: 256 x 208 (total 64512)
 
 // exp2 on the FMA pipe for a pair of values: round-to-nearest
 // range reduction with the 1.5*2^23 magic add, 2^f on f in [-0.5, 0.5] by a degree-3
@@ -285,34 +288,51 @@ __device__ __forceinline__ void exp_row(float* s, float c, float m_use, uint32_t
   sum1 = a1 + b1;
 }
 
-// Mask (diagonal / tail blocks only), row max (T.reduce_max: in-thread, each
-// thread owns one whole S row) and the conditional running-max update of one K/V block.
-// Returns whether the block was masked; m_use is the max the exps subtract (-inf guard).
-__device__ __forceinline__ bool row_max_update(float* s, int k0, int limit, float c, float m,
-                                               float& m_new_out, float& alpha_out, float& m_use_out) {
-  // any column beyond this row's last key? (diagonal / tail blocks only)
-  const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
+// Mask columns [C0, C0+NC) of a diagonal / tail block (k0 + col > limit -> -inf) and
+// return their max (T.reduce_max: in-thread, each thread owns one whole S row).
+template <int C0, int NC>
+__device__ __forceinline__ float mask_max_cols(float* s, int k0, int limit, bool masked) {
   if (masked) {
 #pragma unroll
-    for (int cc = 0; cc < BN; ++cc)
+    for (int cc = C0; cc < C0 + NC; ++cc)
       if (k0 + cc > limit) s[cc] = -INFINITY;
   }
-  float mq[4];
+  constexpr int R = NC / 32;
+  float mq[R];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) mq[r] = fmax3(s[r * 32], s[r * 32 + 1], s[r * 32 + 2]);
+  for (int r = 0; r < R; ++r) mq[r] = fmax3(s[C0 + r * 32], s[C0 + r * 32 + 1], s[C0 + r * 32 + 2]);
 #pragma unroll
   for (int cc = 3; cc + 1 < 32; cc += 2)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) mq[r] = fmax3(mq[r], s[r * 32 + cc], s[r * 32 + cc + 1]);
+    for (int r = 0; r < R; ++r) mq[r] = fmax3(mq[r], s[C0 + r * 32 + cc], s[C0 + r * 32 + cc + 1]);
 #pragma unroll
-  for (int r = 0; r < 4; ++r) mq[r] = fmaxf(mq[r], s[r * 32 + 31]);
-  const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+  for (int r = 0; r < R; ++r) mq[r] = fmaxf(mq[r], s[C0 + r * 32 + 31]);
+  float mx = mq[0];
+#pragma unroll
+  for (int r = 1; r < R; ++r) mx = fmaxf(mx, mq[r]);
+  return mx;
+}
+
+// Conditional running-max update from the block's row max mx (raw score units).
+__device__ __forceinline__ void row_max_finish(float mx, float c, float m, float& m_new_out,
+                                               float& alpha_out, float& m_use_out) {
   const float mxs = (mx == -INFINITY) ? -INFINITY : mx * c;
   const float m_new = (mxs > m + RESCALE_LOG2) ? mxs : m;  // conditional rescale
   const float m_use = (m_new == -INFINITY) ? 0.f : m_new;  // -inf guard
   alpha_out = ex2(m - m_use);                              // scores_scale
   m_new_out = m_new;
   m_use_out = m_use;
+}
+
+// Mask (diagonal / tail blocks only), row max and the conditional running-max update of
+// one K/V block. Returns whether the block was masked; m_use is the max the exps
+// subtract (-inf guard).
+__device__ __forceinline__ bool row_max_update(float* s, int k0, int limit, float c, float m,
+                                               float& m_new_out, float& alpha_out, float& m_use_out) {
+  // any column beyond this row's last key? (diagonal / tail blocks only)
+  const bool masked = __any_sync(0xffffffffu, k0 + BN - 1 > limit);
+  const float mx = mask_max_cols<0, BN>(s, k0, limit, masked);
+  row_max_finish(mx, c, m, m_new_out, alpha_out, m_use_out);
   return masked;
 }
 
