@@ -98,6 +98,24 @@ def test_single_rank_replicated_equals_tl_attn_fwd():
         assert torch.equal(l, lse_ref)
 
 
+def test_eight_outputs_and_no_lse():
+    """The maximum fan-out (8 outputs) with lse_outs = NULL, D = 64 kernel, a shard at a
+    head offset: only the shard's heads are written, the rest of every buffer is untouched."""
+    from paper_2504_17577_b200 import attention, tl_attn_fwd_replicated
+    from paper_2504_17577_b200.inputs import gen_qkv
+    from paper_2504_17577_b200.tlattn import dtype_code
+    B, Hq_total, Hl, Hkvl, S, D = 1, 8, 2, 1, 200, 64
+    q, k, v = gen_qkv(B, Hl, Hkvl, S, S, D, torch.float16, 9, "cuda")
+    o_ref, _ = attention(q, k, v, causal=False)
+    outs = [torch.full((B, S, Hq_total, D), 7.0, dtype=torch.float16, device="cuda") for _ in range(8)]
+    tl_attn_fwd_replicated(q, k, v, outs, None, B, 0, Hq_total, 4, B, Hl, Hkvl, S, S, D, 0,
+                           1.0 / D ** 0.5, dtype_code(q.dtype))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o[:, :, 4:6].view(torch.int16), o_ref.view(torch.int16))
+        assert (o[:, :, :4] == 7.0).all() and (o[:, :, 6:] == 7.0).all()
+
+
 def test_replicated_bad_args():
     from paper_2504_17577_b200 import TlAttnError, tl_attn_fwd_replicated
     q = torch.zeros(1, 128, 2, 128, dtype=torch.bfloat16, device="cuda")
