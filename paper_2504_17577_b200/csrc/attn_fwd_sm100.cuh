@@ -51,6 +51,8 @@ struct AttnParams {
   int n_mblk;        // ceil(Sq / unit rows)
   int n_units;       // B * Hq * n_mblk
   int unit_tiles;    // CTA-pair kernel: query tiles (of 256 rows) per unit, 2 or 1 (short Sq)
+  int lpt;           // unit order: 0 = (b, h)-major (K/V of a head stay in L2), 1 = query-
+                     // block-major, heaviest first over ALL heads (causal, K/V fit in L2)
   unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
   static constexpr bool kRepl = false;
 };
@@ -400,8 +402,9 @@ struct Unit {
 // K/V stay L2-resident (the T.use_swizzle idea).
 __device__ __forceinline__ Unit decode_unit(int u, const AttnParams& p) {
   Unit U;
-  const int mb_i = u % p.n_mblk;
-  const int bh = u / p.n_mblk;
+  const int nbh = p.B * p.Hq;
+  const int mb_i = p.lpt ? u / nbh : u % p.n_mblk;
+  const int bh = p.lpt ? u % nbh : u / p.n_mblk;
   U.h = bh % p.Hq;
   U.b = bh / p.Hq;
   U.m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;

@@ -73,8 +73,10 @@ struct Unit2 {
 
 __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
   Unit2 U;
-  const int mb_i = u % p.n_mblk;  // n_mblk = ceil(Sq / (256 * unit_tiles)) for this kernel
-  const int bh = u / p.n_mblk;
+  // n_mblk = ceil(Sq / (256 * unit_tiles)) for this kernel
+  const int nbh = p.B * p.Hq;
+  const int mb_i = p.lpt ? u / nbh : u % p.n_mblk;
+  const int bh = p.lpt ? u % nbh : u / p.n_mblk;
   U.h = bh % p.Hq;
   U.b = bh / p.Hq;
   const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;

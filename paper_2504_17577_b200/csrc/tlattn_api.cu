@@ -245,6 +245,17 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
   }
   const int unit_rows = pair ? 2 * BM * prm.unit_tiles : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
+  // Unit order (the T.use_swizzle idea). Default: units of one (b, kv head) are
+  // adjacent so their K/V stay L2-resident. Causal problems whose whole K/V fits in half of
+  // the 126 MB L2 (the paper's Table 3 shapes) instead run the heaviest query blocks of ALL
+  // heads first (longest-processing-time order), so the last wave is not one head's long
+  // unit starting late.
+  const double kv_bytes = 4.0 * B * Hkv * (double)Skv * D;
+  prm.lpt = (causal && kv_bytes <= 64.0 * (1 << 20)) ? 1 : 0;
+  if (const char* e = std::getenv("TLATTN_LPT")) {  // A/B experiments only
+    const int v = std::atoi(e);
+    if (v == 0 || v == 1) prm.lpt = v;
+  }
   prm.n_units = B * Hq * prm.n_mblk;  // bounded in validate()
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
