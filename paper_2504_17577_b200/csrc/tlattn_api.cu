@@ -246,12 +246,20 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
   const int unit_rows = pair ? 2 * BM * prm.unit_tiles : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
   // Unit order (the T.use_swizzle idea). Default: units of one (b, kv head) are
-  // adjacent so their K/V stay L2-resident. Causal problems whose whole K/V fits in half of
-  // the 126 MB L2 (the paper's Table 3 shapes) instead run the heaviest query blocks of ALL
-  // heads first (longest-processing-time order), so the last wave is not one head's long
-  // unit starting late.
+  // adjacent so their K/V stay L2-resident. Causal problems instead run the heaviest query
+  // blocks of ALL heads first (longest-processing-time order) when either their whole K/V
+  // fits in half of the 126 MB L2 (the paper's Table 3 shapes), or the heaviest unit is
+  // >= 5 % of one worker's share of the work (long sequences: the last head's first unit
+  // would otherwise start late and run alone). Measured: Table 3 FA4 +26 %,
+  // C4 +12.6 %, C3 +1.4 %; C5 (short sequences, 2 GB of K/V) -5 %, so it keeps head-major.
   const double kv_bytes = 4.0 * B * Hkv * (double)Skv * D;
-  prm.lpt = (causal && kv_bytes <= 64.0 * (1 << 20)) ? 1 : 0;
+  const int workers = pair ? di->sm_count / 2 : di->sm_count;
+  const double nb = std::ceil(Skv / 128.0);                    // K/V blocks of a full row
+  const double tile_rows = pair ? 256.0 : 128.0;
+  const double tiles_per_unit = pair ? prm.unit_tiles : TILES;
+  const double heaviest = tiles_per_unit * nb;                 // tile-blocks of the top unit
+  const double share = (double)B * Hq * std::ceil(Sq / tile_rows) * nb * 0.5 / workers;
+  prm.lpt = (causal && (kv_bytes <= 64.0 * (1 << 20) || heaviest >= 0.05 * share)) ? 1 : 0;
   if (const char* e = std::getenv("TLATTN_LPT")) {  // A/B experiments only
     const int v = std::atoi(e);
     if (v == 0 || v == 1) prm.lpt = v;
