@@ -218,8 +218,8 @@ struct Exp2Poly {
 };
 
 // Column pairs (of 64 per row) whose exp2 runs on the FMA pipe instead of MUFU: EMU of
-// every 8. Measured on B200: D=64 gains from EMU=3 (the softmax
-// bounds that shape), D=128 is fastest with EMU=0 (the extra issue slots cost more than
+// every 8. Measured on B200: D=64 gains from EMU=2 (the softmax
+// bounds that shape; TLATTN_EMU64), D=128 is fastest with EMU=0 (the extra issue slots cost more than
 // the MUFU time saved).
 // TLATTN_EXP_VARIANT (experiments only): 0 = per-kernel EMU, 1 = none, 2 = all,
 // 3 = no exp at all (timing of everything else; WRONG results).
@@ -230,6 +230,12 @@ struct Exp2Poly {
 #define TLATTN_EMU_2SM TLATTN_EMU_OVERRIDE
 #else
 #define TLATTN_EMU_2SM 0
+#endif
+// exp2 offload of the D = 64 kernel: EMU of every 8 column pairs on the FMA pipe. Measured
+// with P in TMEM and the LPT order (B200, same box): EMU 1/2/3 -> C4 779 / 811 / 763,
+// D=64 non-causal 760 / 805 / 740 TFLOP/s, so 2.
+#ifndef TLATTN_EMU64
+#define TLATTN_EMU64 2
 #endif
 template <int EMU>
 __host__ __device__ constexpr bool emu_pair(int q) {
@@ -703,7 +709,7 @@ tl_attn_fwd_kernel(const __grid_constant__ PT p) {
 
         float m_new, alpha, sum;
         uint32_t pk[BN / 2];
-        softmax_row_block<BF16, (D == 64 ? 3 : 0)>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
+        softmax_row_block<BF16, (D == 64 ? TLATTN_EMU64 : 0)>(sr, j * BN, limit, c, m, m_new, alpha, sum, pk);
         if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * (j & 15) + 2);
         if (j > 0) {
           // O_t must hold PV_t(j-1) before it is rescaled and before P_t smem is reused
