@@ -37,6 +37,19 @@ constexpr int SOFTMAX_WARP0 = 4;   // warps 4..11
 constexpr int CHUNK_BYTES = 128 * 128;  // one 128-row x 64-element 16-bit SW128 box
 constexpr uint32_t TMEM_COLS = 512;
 
+// Division by a runtime constant without the MUFU.RCP of the generic integer divide (the
+// softmax warps keep MUFU saturated, so a unit decode with five divides cost ~1200 clocks
+// in the MMA issuer's unit transition, profiles/r01_trace_notes.md): for 0 <= n < 2^31,
+// n / d = (umulhi(n, mul) + n) >> shr with shr = ceil(log2 d) and
+// mul = floor(2^32 (2^shr - d) / d) + 1 (host-computed, make_fastdiv).
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __device__ __forceinline__ int div(int n) const {
+    return static_cast<int>((__umulhi(static_cast<uint32_t>(n), mul) + static_cast<uint32_t>(n)) >> shr);
+  }
+  __device__ __forceinline__ int mod(int n) const { return n - div(n) * static_cast<int>(d); }
+};
+
 struct AttnParams {
   CUtensorMap tm_q;  // BSHD as 4-D (D, Hq, Sq, B), box (64, 1, 128, 1), SWIZZLE_128B
   CUtensorMap tm_k;  // (D, Hkv, Skv, B)
@@ -51,6 +64,7 @@ struct AttnParams {
   int n_mblk;        // ceil(Sq / unit rows)
   int n_units;       // B * Hq * n_mblk
   int unit_tiles;    // CTA-pair kernel: query tiles (of 256 rows) per unit, 2 or 1 (short Sq)
+  FastDiv fd_mblk, fd_nbh, fd_hq, fd_grp;  // / n_mblk, / (B Hq), / Hq, / (Hq / Hkv)
   int lpt;           // unit order: 0 = (b, h)-major (K/V of a head stay in L2), 1 = query-
                      // block-major, heaviest first over ALL heads (causal, K/V fit in L2)
   unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
@@ -408,13 +422,12 @@ struct Unit {
 // K/V stay L2-resident (the T.use_swizzle idea).
 __device__ __forceinline__ Unit decode_unit(int u, const AttnParams& p) {
   Unit U;
-  const int nbh = p.B * p.Hq;
-  const int mb_i = p.lpt ? u / nbh : u % p.n_mblk;
-  const int bh = p.lpt ? u % nbh : u / p.n_mblk;
-  U.h = bh % p.Hq;
-  U.b = bh / p.Hq;
+  const int mb_i = p.lpt ? p.fd_nbh.div(u) : p.fd_mblk.mod(u);
+  const int bh = p.lpt ? p.fd_nbh.mod(u) : p.fd_mblk.div(u);
+  U.b = p.fd_hq.div(bh);
+  U.h = bh - U.b * p.Hq;
   U.m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
-  U.hkv = U.h / (p.Hq / p.Hkv);  // GQA grouping
+  U.hkv = p.fd_grp.div(U.h);  // GQA grouping h / (Hq / Hkv)
   U.n0 = tile_nblocks(U.m_blk * (TILES * BM), p);
   U.n1 = tile_nblocks(U.m_blk * (TILES * BM) + BM, p);
   return U;

@@ -74,13 +74,12 @@ struct Unit2 {
 __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
   Unit2 U;
   // n_mblk = ceil(Sq / (256 * unit_tiles)) for this kernel
-  const int nbh = p.B * p.Hq;
-  const int mb_i = p.lpt ? u / nbh : u % p.n_mblk;
-  const int bh = p.lpt ? u % nbh : u / p.n_mblk;
-  U.h = bh % p.Hq;
-  U.b = bh / p.Hq;
+  const int mb_i = p.lpt ? p.fd_nbh.div(u) : p.fd_mblk.mod(u);
+  const int bh = p.lpt ? p.fd_nbh.mod(u) : p.fd_mblk.div(u);
+  U.b = p.fd_hq.div(bh);
+  U.h = bh - U.b * p.Hq;
   const int m_blk = p.causal ? (p.n_mblk - 1 - mb_i) : mb_i;
-  U.hkv = U.h / (p.Hq / p.Hkv);  // GQA grouping
+  U.hkv = p.fd_grp.div(U.h);  // GQA grouping h / (Hq / Hkv)
   U.tiles = p.unit_tiles;
   U.r0 = m_blk * (2 * BM) * p.unit_tiles;
   U.n0 = tile_nblocks_rows(U.r0, 2 * BM, p);
@@ -240,6 +239,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
           auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
           mbar_wait(bar_q_full, k & 1);
+          TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 7);  // Q ready (unit start)
           auto issue_s = [&](int j) {
             const int sl = kpos(j) % C::NST;
             TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 0);
@@ -311,6 +311,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
             mma_commit_2sm(bar_kv_empty(sl));
           }
+          TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 6);  // issuer done with the unit's MMAs
           mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
           const int nxt = clc_query(sSched + 16 * (k & 1));
           mbar_arrive(bar_sched_empty(k & 1));

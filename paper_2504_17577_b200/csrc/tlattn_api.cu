@@ -203,6 +203,16 @@ int launch(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
   return TL_OK;
 }
 
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;  // ceil(log2 d)
+  f.shr = l;
+  f.mul = static_cast<uint32_t>(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  return f;
+}
+
 // Shared by tl_attn_fwd and tl_attn_fwd_replicated: input tensor maps, sizes, unit
 // geometry; then the launch of the kernel instantiated for the parameter type PT.
 template <class PT>
@@ -265,6 +275,10 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
     if (v == 0 || v == 1) prm.lpt = v;
   }
   prm.n_units = B * Hq * prm.n_mblk;  // bounded in validate()
+  prm.fd_mblk = make_fastdiv(prm.n_mblk);
+  prm.fd_nbh = make_fastdiv(B * Hq);
+  prm.fd_hq = make_fastdiv(Hq);
+  prm.fd_grp = make_fastdiv(Hq / Hkv);
   // Negative scale: the tensor core negates Q (instruction-descriptor a_negate), so the
   // kernel computes S' = -QK^T and uses c = |scale| log2(e) >= 0; scale*S == |scale|*S'.
   prm.neg = scale < 0.f ? 1 : 0;

@@ -21,7 +21,8 @@ tr = buf.cpu().tolist()
 t0 = min(x for x in tr[:8000] if x)
 f = lambda x: f"{x - t0:7d}" if x else "      -"
 for kk in range(nunits):
-    print(f"--- unit {kk}")
+    g = lambda t, e: f(tr[200 * kk + 4000 + 1000 * t + 8 * 15 + e])
+    print(f"--- unit {kk}: issuer Q-ready t0 {g(0, 7)} t1 {g(1, 7)} | issuer done t0 {g(0, 6)} t1 {g(1, 6)}")
     for j in range(16):
         rows = []
         for t in (0, 1):
