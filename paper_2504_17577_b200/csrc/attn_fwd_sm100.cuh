@@ -196,8 +196,13 @@ constexpr float RESCALE_LOG2 = 8.0f;
 // The CTA is launched with 168 x 384 = 64512 registers (__launch_bounds__(384, 1)); the
 // split must fit that pool (216 for the softmax warpgroups would need 65536 and blocks
 // setmaxnreg.inc forever — measured: the watchdog traps).
-constexpr uint32_t REGS_SMALL = 88;     // warpgroup 0: 128 x 88
-constexpr uint32_t REGS_SOFTMAX = 208;  // warpgroups 1-2: 256 x 208 (total 64512)
+#ifndef TLATTN_REGS_SMALL  // experiments may override the split (must fit 64512)
+#define TLATTN_REGS_SMALL 88
+#define TLATTN_REGS_SOFTMAX 208
+#endif
+constexpr uint32_t REGS_SMALL = TLATTN_REGS_SMALL;      // warpgroup 0: 128 x 88
+constexpr uint32_t REGS_SOFTMAX = TLATTN_REGS_SOFTMAX;  // warpgroups 1-2: 256 x 208 (total 64512)
+static_assert(128 * REGS_SMALL + 256 * REGS_SOFTMAX <= 64512, "register split exceeds the launch pool");
 
 // exp2 on the FMA pipe for a pair of values: round-to-nearest
 // range reduction with the 1.5*2^23 magic add, 2^f on f in [-0.5, 0.5] by a degree-3
