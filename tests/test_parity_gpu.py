@@ -257,3 +257,24 @@ def test_concurrent_streams():
         ob = attention(*b, causal=False)
     torch.cuda.synchronize()
     assert torch.equal(oa[0], ra[0]) and torch.equal(ob[0], rb[0])
+
+
+@pytest.mark.parametrize("D,dtype", [(128, BF), (64, F16)])
+def test_unit_order_does_not_change_results(D, dtype, monkeypatch):
+    """The LPT (query-block-major) and the (b, h)-major unit orders schedule the same
+    units differently over persistent CTAs that each run several units; every unit's
+    arithmetic is the same, so O and LSE must be bitwise equal. Both orders are also
+    checked against the oracle on sampled rows."""
+    from _parity import sample_rows
+    B, Hq, Hkv, S = 4, 16, 4, 2048  # 256 pair units / 512 single-CTA units: several per CTA
+    q, k, v = gen(B, Hq, Hkv, S, S, D, dtype, 303 + D)
+    outs = {}
+    for order in ("0", "1"):
+        monkeypatch.setenv("TLATTN_LPT", order)
+        outs[order] = attention(q, k, v, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(outs["0"][0].view(torch.int16), outs["1"][0].view(torch.int16))
+    assert torch.equal(outs["0"][1], outs["1"][1])
+    rows = sample_rows(S, np.random.default_rng(D), extra=64)
+    check_against_oracle(q, k, v, True, default_scale(D), rows_per_head=rows,
+                         label=f"LPT D{D}", full_rows_heads=((0, 0),))
