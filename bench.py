@@ -363,6 +363,9 @@ def run_ours(args, world, rank, local):
             if name == cfg.name:
                 continue
             extra[name] = bench_one(CONFIGS[name], pk, steps=max(5, min(args.steps, 20)))
+        from paper_2504_17577_b200.configs import PAPER_T3
+        for name in ("FA3", "FA4"):  # the paper's own FlashAttention shapes (Table 3)
+            extra["paper_" + name] = bench_one(PAPER_T3[name], pk, steps=max(5, min(args.steps, 20)))
         for gname in ("M5", "M2"):  # the paper's GEMM on Table 2 shapes
             extra["gemm_" + gname] = bench_gemm(gname, pk)
         from paper_2504_17577_b200.configs import MLA_CONFIGS
