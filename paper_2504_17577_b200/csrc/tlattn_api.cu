@@ -32,7 +32,9 @@ struct DeviceInfo {
   int sm_count = 0;
   int major = 0, minor = 0;
   bool ok = false;
-  bool smem_set[16] = {};
+  // per kernel instantiation: cudaFuncAttributeMaxDynamicSharedMemorySize already set.
+  // Slots: attention 0-5, replicated-output attention 8-13, GEMM 16-17.
+  bool smem_set[32] = {};
 };
 
 constexpr int kMaxDevices = 64;
@@ -286,7 +288,7 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool bf = dtype == TL_DTYPE_BF16;
-  const int i0 = PT::kRepl ? 6 : 0;  // per-instantiation "smem attribute set" slots
+  const int i0 = PT::kRepl ? 8 : 0;  // per-instantiation "smem attribute set" slots
   if (pair) rc = bf ? launch_2sm<true>(prm, *di, i0 + 4, st) : launch_2sm<false>(prm, *di, i0 + 5, st);
   else if (D == 128) rc = bf ? launch<128, true>(prm, *di, i0 + 0, st) : launch<128, false>(prm, *di, i0 + 1, st);
   else rc = bf ? launch<64, true>(prm, *di, i0 + 2, st) : launch<64, false>(prm, *di, i0 + 3, st);
@@ -636,7 +638,7 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
   prm.tiles_n = (N + 255) / 256;
   prm.group_n = 8;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  rc = dtype == TL_DTYPE_BF16 ? launch_gemm<true>(prm, *di, 6, st) : launch_gemm<false>(prm, *di, 7, st);
+  rc = dtype == TL_DTYPE_BF16 ? launch_gemm<true>(prm, *di, 16, st) : launch_gemm<false>(prm, *di, 17, st);
   if (rc == TL_OK) g_last_launches = 1;
   return rc;
 }
