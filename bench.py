@@ -366,7 +366,7 @@ def run_ours(args, world, rank, local):
         from paper_2504_17577_b200.configs import PAPER_T3
         for name in ("FA3", "FA4"):  # the paper's own FlashAttention shapes (Table 3)
             extra["paper_" + name] = bench_one(PAPER_T3[name], pk, steps=max(5, min(args.steps, 20)))
-        for gname in ("M5", "M2"):  # the paper's GEMM on Table 2 shapes
+        for gname in ("M5", "M2", "V1", "V4"):  # the paper's GEMM on Table 2 shapes
             extra["gemm_" + gname] = bench_gemm(gname, pk)
         from paper_2504_17577_b200.configs import MLA_CONFIGS
         for mc in MLA_CONFIGS:  # MLA decode (Fig. 18)
@@ -482,7 +482,8 @@ def bench_mla(cfg, pk, steps=20, warmup=3):
     return res
 
 
-GEMM_TABLE2 = {"M2": (4096, 28672, 8192), "M5": (8192, 8192, 8192)}  # PAPER.md Table 2
+GEMM_TABLE2 = {"M2": (4096, 28672, 8192), "M5": (8192, 8192, 8192),  # PAPER.md Table 2
+               "V1": (1, 43008, 14336), "V4": (1, 14336, 57344)}     # GEMV rows (HBM-bound)
 
 
 def bench_gemm(name, pk, iters=10):
@@ -512,9 +513,14 @@ def bench_gemm(name, pk, iters=10):
     fl = 2.0 * M * N * K
     del a, b, c
     torch.cuda.empty_cache()
-    return {"shape": [M, N, K], "tflops": fl / t / 1e9, "kernel_ms": t,
-            "frac_of_peak": fl / t / 1e9 / pk["burst"], "cublas_tflops": fl / tc / 1e9,
-            "vs_cublas": tc / t}
+    res = {"shape": [M, N, K], "tflops": fl / t / 1e9, "kernel_ms": t,
+           "frac_of_peak": fl / t / 1e9 / pk["burst"], "cublas_tflops": fl / tc / 1e9,
+           "vs_cublas": tc / t}
+    if M == 1:  # GEMV: HBM-bound, the roofline is the copy bandwidth
+        by = 2.0 * (K + K * N + N)
+        res.update({"bound": "hbm", "hbm_gbs": by / t / 1e6, "frac_of_hbm": by / t / 1e6 / pk["hbm"],
+                    "cublas_hbm_gbs": by / tc / 1e6})
+    return res
 
 
 def main():

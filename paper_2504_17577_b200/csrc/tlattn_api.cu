@@ -19,6 +19,7 @@
 #include "attn_fwd_sm100.cuh"
 #include "attn_fwd_sm100_2sm.cuh"
 #include "gemm_sm100_2sm.cuh"
+#include "gemv_sm100.cuh"
 #include "mla_decode_sm100.cuh"
 
 using namespace tlattn;
@@ -623,6 +624,28 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
   int dev, rc;
   DeviceInfo* di;
   if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  if (M == 1) {
+    // GEMV (Table 2 "V" shapes): HBM-bound, no tensor cores (gemv_sm100.cuh). Column
+    // tiles of tc <= 256 so that (N / tc) clusters of 8 CTAs give >= ~2 CTAs per SM.
+    GemvParams gp;
+    gp.a = static_cast<const uint16_t*>(a);
+    gp.b = static_cast<const uint16_t*>(b);
+    gp.c = static_cast<uint16_t*>(c);
+    gp.N = N;
+    gp.K = K;
+    int tc = 256;
+    while (tc > 32 && (N + tc - 1) / tc < 37) tc /= 2;
+    gp.tc = tc;
+    const long long tiles = (N + tc - 1) / tc;
+    if (tiles > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const dim3 grid(static_cast<unsigned>(tiles), GEMV_CS, 1);
+    if (dtype == TL_DTYPE_BF16) tl_gemv_kernel<true><<<grid, GEMV_THREADS, 0, st>>>(gp);
+    else tl_gemv_kernel<false><<<grid, GEMV_THREADS, 0, st>>>(gp);
+    if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+    g_last_launches = 1;
+    return TL_OK;
+  }
   auto enc = get_encode();
   if (!enc) return TL_ERR_CUDA;
   GemmParams prm;

@@ -17,6 +17,11 @@ TABLE2 = {  # PAPER.md Table 2: name -> (m, n, k)
     "M3": (4096, 8192, 28672), "M4": (8192, 1024, 8192), "M5": (8192, 8192, 8192),
     "M6": (8192, 28672, 8192), "M7": (8192, 8192, 28672),
 }
+TABLE2_V = {  # the GEMV rows of Table 2 (m = 1): tl_gemm's M = 1 path (gemv_sm100.cuh)
+    "V0": (1, 16384, 16384), "V1": (1, 43008, 14336), "V2": (1, 14336, 14336),
+    "V3": (1, 57344, 14336), "V4": (1, 14336, 57344), "V5": (1, 9216, 9216),
+    "V6": (1, 36864, 9216), "V7": (1, 9216, 36864),
+}
 
 
 def make(M, N, K, dt, seed):
@@ -80,3 +85,31 @@ def test_gemm_bad_args():
     with pytest.raises(TlAttnError) as e:
         gemm(a, b)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("N,K,dt", [
+    (264, 1000, torch.bfloat16),    # ragged K split over the cluster, N below one tile
+    (8192, 1000, torch.float16),    # K split with ragged 8-row load groups
+    (1000, 8, torch.bfloat16),      # one row per CTA of the K split at most
+    (57344, 64, torch.float16),     # many column tiles
+])
+def test_gemv_parity(N, K, dt):
+    """M = 1 (GEMV path): every output element against the fp64 oracle."""
+    a, b = make(1, N, K, dt, 31 + N + K)
+    c = gemm(a, b)
+    torch.cuda.synchronize()
+    assert tl_attn_last_launch_count() == 1
+    check(a, b, c, [0])
+
+
+@pytest.mark.parametrize("name", sorted(TABLE2_V))
+def test_gemv_table2_shapes(name):
+    """The paper's GEMV shapes at full size, every output element."""
+    M, N, K = TABLE2_V[name]
+    a, b = make(M, N, K, torch.bfloat16, 77)
+    c = gemm(a, b)
+    torch.cuda.synchronize()
+    check(a, b, c, [0])
+    del a, b, c
+    torch.cuda.empty_cache()
+
