@@ -110,6 +110,10 @@ uint64_t tl_attn_host_workspace_bytes(int B, int Hq, int Hkv, int Sq, int Skv, i
  *   dtype  TL_DTYPE_F16 or TL_DTYPE_BF16; accumulation is fp32, C is rounded RN
  *   stream cudaStream_t as void*
  *
+ * M = 1 (the GEMV rows of Table 2) runs an HBM-bound kernel instead of the tensor-core
+ * tiles: clusters of 8 CTAs split K and reduce through distributed shared memory in a
+ * fixed order (deterministic). Both paths are one kernel launch.
+ *
  * Ownership / synchronisation as tl_attn_fwd (caller-owned buffers, stream-ordered, no
  * allocation, graph-capturable). c must not alias a or b.
  * Errors: TL_ERR_INVALID_VALUE (NULL pointer, size < 1, bad dtype), TL_ERR_UNSUPPORTED
