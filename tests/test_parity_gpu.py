@@ -278,3 +278,30 @@ def test_unit_order_does_not_change_results(D, dtype, monkeypatch):
     rows = sample_rows(S, np.random.default_rng(D), extra=64)
     check_against_oracle(q, k, v, True, default_scale(D), rows_per_head=rows,
                          label=f"LPT D{D}", full_rows_heads=((0, 0),))
+
+
+def _fuzz_cases(n=40, seed=2504):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        D = int(rng.choice([64, 128]))
+        dtype = [BF, F16][int(rng.integers(2))]
+        Hkv = int(rng.choice([1, 2, 3]))
+        Hq = Hkv * int(rng.choice([1, 2, 4]))
+        B = int(rng.integers(1, 4))
+        Sq = int(rng.integers(1, 1300))
+        Skv = Sq if rng.random() < 0.5 else int(rng.integers(1, 1300))
+        causal = bool(rng.random() < 0.6)
+        cases.append((B, Hq, Hkv, Sq, Skv, D, dtype, causal))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: "B{}H{}/{}S{}x{}D{}{}{}".format(
+    c[0], c[1], c[2], c[3], c[4], c[5], "bf" if c[6] == BF else "h", "c" if c[7] else ""))
+def test_parity_fuzz(case):
+    """Seeded random shapes (batch, GQA ratio, ragged Sq / Skv, Sq != Skv, D, dtype, causal):
+    every element against the oracle, through whichever kernel, unit mode and unit order the
+    launcher picks for the shape."""
+    B, Hq, Hkv, Sq, Skv, D, dtype, causal = case
+    q, k, v = gen(B, Hq, Hkv, Sq, Skv, D, dtype, 9000 + Sq * 7 + Skv)
+    check_against_oracle(q, k, v, causal, default_scale(D), label=str(case))
