@@ -626,7 +626,8 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
   if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
   if (M == 1) {
     // GEMV (Table 2 "V" shapes): HBM-bound, no tensor cores (gemv_sm100.cuh). Column
-    // tiles of tc <= 256 so that (N / tc) clusters of 8 CTAs give >= ~2 CTAs per SM.
+    // tiles of 256 (narrower only when fewer than 18 tiles = 144 CTAs): measured on the V
+    // shapes, 256 is best or within noise except N = 36864 (128: +5 %).
     GemvParams gp;
     gp.a = static_cast<const uint16_t*>(a);
     gp.b = static_cast<const uint16_t*>(b);
@@ -634,7 +635,11 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
     gp.N = N;
     gp.K = K;
     int tc = 256;
-    while (tc > 32 && (N + tc - 1) / tc < 37) tc /= 2;
+    while (tc > 32 && (N + tc - 1) / tc < 18) tc /= 2;
+    if (const char* e = std::getenv("TLATTN_GEMV_TC")) {  // A/B experiments only
+      const int v = std::atoi(e);
+      if (v == 32 || v == 64 || v == 128 || v == 256) tc = v;
+    }
     gp.tc = tc;
     const long long tiles = (N + tc - 1) / tc;
     if (tiles > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
