@@ -383,6 +383,8 @@ def run_ours(args, world, rank, local):
                 "dtype": cfg.dtype_name, "data": "synthetic",
                 "config": {**cfg.as_dict(), "parallelism": f"{args.shard}-shard x{world}",
                            "flop_per_step": flop, "flop_convention": "4*B*Hq*Sq*Skv*D, x1/2 causal",
+                           "exact_flop_per_step": cfg.flops_exact(),
+                           "exact_tflops": cfg.flops_exact() / (ms * 1e-3) / 1e12,
                            "l2": "inputs > 126 MB L2 (no flush)"},
                 "frac_of_peak": value / pk["burst"],
                 "roofline": roofline,
