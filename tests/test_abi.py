@@ -135,3 +135,48 @@ def test_mla_without_device(lib):
     assert mla_call(lib) == 3  # arguments valid, no device -> TL_ERR_CUDA (no fallback)
     assert tlattn.tl_mla_decode_workspace_bytes(2, 128, 1) == 0  # needs the device's SM count
     assert tlattn.tl_mla_decode_workspace_bytes(0, 128, 1) == 0
+
+
+# ------------------------------------------- replicated output / peer memory
+def _ptrs(*xs):
+    arr = (ctypes.c_void_p * len(xs))(*xs)
+    return ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+
+
+REP_GOOD = dict(q=FAKE, k=FAKE, v=FAKE, outs=[FAKE, FAKE], lses=None, B_total=2, b_off=0,
+                Hq_total=4, h_off=2, B=2, Hq=2, Hkv=1, Sq=128, Skv=128, D=128, causal=1,
+                scale=0.1, dtype=1)
+
+
+def rep_call(lib, **over):
+    a = dict(REP_GOOD, **over)
+    outs = _ptrs(*a["outs"]) if a["outs"] is not None else None
+    lses = _ptrs(*a["lses"]) if a["lses"] is not None else None
+    n = a.get("n", len(a["outs"]) if a["outs"] is not None else 1)
+    return lib.tl_attn_fwd_replicated(a["q"], a["k"], a["v"], outs, lses, n, a["B_total"],
+                                      a["b_off"], a["Hq_total"], a["h_off"], a["B"], a["Hq"],
+                                      a["Hkv"], a["Sq"], a["Skv"], a["D"], a["causal"], a["scale"],
+                                      a["dtype"], None)
+
+
+@pytest.mark.parametrize("over,code", [
+    (dict(outs=None), 1), (dict(n=0), 1), (dict(outs=[FAKE] * 9), 1), (dict(outs=[FAKE, 0]), 1),
+    (dict(h_off=3), 1), (dict(b_off=1), 1), (dict(h_off=-1), 1), (dict(Hq_total=0), 1),
+    (dict(q=None), 1), (dict(D=96), 2), (dict(outs=[FAKE, FAKE + 8]), 2),
+    (dict(lses=[FAKE, FAKE + 2]), 2),
+])
+def test_replicated_invalid_arguments_rejected(lib, over, code):
+    assert rep_call(lib, **over) == code
+
+
+def test_peer_barrier_and_ipc_invalid_arguments_rejected(lib):
+    assert lib.tl_peer_barrier(None, 2, 0, 1, None) == 1
+    assert lib.tl_peer_barrier(_ptrs(FAKE, FAKE), 0, 0, 1, None) == 1
+    assert lib.tl_peer_barrier(_ptrs(*([FAKE] * 9)), 9, 0, 1, None) == 1
+    assert lib.tl_peer_barrier(_ptrs(FAKE, FAKE), 2, 2, 1, None) == 1
+    assert lib.tl_peer_barrier(_ptrs(FAKE, FAKE + 2), 2, 0, 1, None) == 1
+    assert lib.tl_ipc_handle_bytes() >= 64
+    buf = ctypes.create_string_buffer(lib.tl_ipc_handle_bytes())
+    assert lib.tl_ipc_get_handle(None, buf) == 1
+    assert lib.tl_ipc_open_handle(None, None) == 1
+    assert lib.tl_ipc_close_handle(None) == 1
