@@ -170,14 +170,14 @@ def gemm_rows(a, b, dtype, rows):
 def gemm_rows_parallel(a, b, dtype, rows, threads=None):
     threads = threads or len(os.sched_getaffinity(0))
     rows = list(rows)
-    chunks = [rows[i::threads] for i in range(threads) if rows[i::threads]]
+    # chunks of POSITIONS (a row index may repeat; each position gets its own result)
+    pos_chunks = [list(range(i, len(rows), threads)) for i in range(threads) if i < len(rows)]
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        res = list(ex.map(lambda r: gemm_rows(a, b, dtype, r), chunks))
+        res = list(ex.map(lambda ps: gemm_rows(a, b, dtype, [rows[p] for p in ps]), pos_chunks))
     out = np.zeros((len(rows), b.shape[1]), np.float64)
-    pos = {r: i for i, r in enumerate(rows)}
-    for ch, c in zip(chunks, res):
-        for k, r in enumerate(ch):
-            out[pos[r]] = c[k]
+    for ps, c in zip(pos_chunks, res):
+        for k, p in enumerate(ps):
+            out[p] = c[k]
     return out
 
 

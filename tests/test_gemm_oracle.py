@@ -58,3 +58,13 @@ def test_parallel_rows_and_bad_args():
                           oracle.gemm_rows(a, b, oracle.ORACLE_BF16, rows))
     with pytest.raises(ValueError):
         oracle.gemm_rows(a, b, oracle.ORACLE_BF16, [20])
+
+
+def test_parallel_rows_keep_positions_of_repeated_rows():
+    """gemm_rows_parallel returns one result per requested position (repeats included)."""
+    rng = np.random.default_rng(3)
+    a = bits(rng.standard_normal((3, 16)), torch.bfloat16)
+    b = bits(rng.standard_normal((16, 8)), torch.bfloat16)
+    got = oracle.gemm_rows_parallel(a, b, oracle.ORACLE_BF16, [2, 0, 2, 2], threads=3)
+    one = oracle.gemm_rows(a, b, oracle.ORACLE_BF16, [2, 0])
+    assert np.array_equal(got, one[[0, 1, 0, 0]])
