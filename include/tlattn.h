@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TLATTN_VERSION 0x000100 /* 0.1.0 */
+#define TLATTN_VERSION 0x000200 /* 0.2.0: + tl_attn_fwd_replicated, tl_peer_barrier, tl_ipc_*; tl_gemm M = 1 path */
 
 enum tl_dtype { TL_DTYPE_F16 = 0, TL_DTYPE_BF16 = 1 };
 

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_version_and_strerror(lib):
-    assert tlattn.tl_attn_version() == 0x000100
+    assert tlattn.tl_attn_version() == 0x000200
     for code in (0, 1, 2, 3):
         assert tlattn.tl_attn_strerror(code).startswith(("TL_OK", "TL_ERR"))
     assert "unknown" in tlattn.tl_attn_strerror(99)
