@@ -626,15 +626,15 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
   if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
   if (M == 1) {
     // GEMV (Table 2 "V" shapes): HBM-bound, no tensor cores (gemv_sm100.cuh). Column
-    // tiles of 256 (narrower only when fewer than 18 tiles = 144 CTAs): measured on the V
-    // shapes, 256 is best or within noise except N = 36864 (128: +5 %).
+    // tiles of 256 (128 for N >= 32768; narrower only when fewer than 18 tiles = 144 CTAs),
+    // the best of 32/64/128/256 measured on the V shapes.
     GemvParams gp;
     gp.a = static_cast<const uint16_t*>(a);
     gp.b = static_cast<const uint16_t*>(b);
     gp.c = static_cast<uint16_t*>(c);
     gp.N = N;
     gp.K = K;
-    int tc = 256;
+    int tc = N >= 32768 ? 128 : 256;  // measured: 128 is 4-5 % faster for N >= 32768
     while (tc > 32 && (N + tc - 1) / tc < 18) tc /= 2;
     if (const char* e = std::getenv("TLATTN_GEMV_TC")) {  // A/B experiments only
       const int v = std::atoi(e);
