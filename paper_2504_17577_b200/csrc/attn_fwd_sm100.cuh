@@ -147,7 +147,10 @@ struct KCfg {
   static constexpr int NST = TLATTN_NST_OVERRIDE;
   static constexpr int P_TILE_BYTES = 0;
 #else
-  static constexpr int NST = (D == 128) ? 3 : (P_TMEM ? 10 : 6);
+#ifndef TLATTN_NST64
+#define TLATTN_NST64 10
+#endif
+  static constexpr int NST = (D == 128) ? 3 : (P_TMEM ? TLATTN_NST64 : 6);
   static constexpr int P_TILE_BYTES = P_TMEM ? 0 : BM * BN * 2;
 #endif
   static constexpr int OFF_Q = 0;
