@@ -28,3 +28,18 @@ def test_config_parity(name):
         stats, _ = check_against_oracle(q, k, v, cfg.causal, cfg.scale, rows_per_head=rows,
                                         label=name, full_rows_heads=full)
     print(name, stats)
+
+
+@pytest.mark.parametrize("name", ["FA0", "FA1", "FA2", "FA3", "FA4"])
+def test_paper_table3_parity(name):
+    """The paper's own FlashAttention shapes (Table 3; reading R13: 32 heads),
+    in the launch configuration the launcher picks for them (short-sequence pair units for
+    S = 512, the LPT unit order for the causal ones): sampled rows of every head and all
+    rows of two heads against the oracle."""
+    from paper_2504_17577_b200.configs import PAPER_T3
+    cfg = PAPER_T3[name]
+    q, k, v = gen(cfg.B, cfg.Hq, cfg.Hkv, cfg.Sq, cfg.Skv, cfg.D, cfg.dtype, cfg.seed)
+    rows = sample_rows(cfg.Sq, np.random.default_rng(cfg.seed), extra=64)
+    stats, _ = check_against_oracle(q, k, v, cfg.causal, cfg.scale, rows_per_head=rows,
+                                    label=name, full_rows_heads=((0, 0), (0, cfg.Hq - 1)))
+    print(name, stats)
