@@ -2,7 +2,9 @@
 """Benchmark: fused attention forward TFLOP/s on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  (N > 1: launched by torch.distributed.run, one rank per GPU, NCCL.)
+  (N > 1: one rank per GPU over NCCL; launched by torch.distributed.run, or — when no
+  WORLD_SIZE is set — bench.py starts the N ranks itself the same way. A world size that
+  differs from --gpus is an error.)
 
 A step = one tl_attn_fwd over this rank's shard of the workload (the whole hot path:
 TMA loads, QK^T, online softmax, PV, epilogue — one kernel launch). Workload: C5
@@ -122,16 +124,40 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """--gpus N > 1 without a torchrun environment: start the N ranks ourselves (one
+    process per GPU, rendezvous on 127.0.0.1) under torch.distributed.run and return its
+    exit code. The launched command is the driver's own form: `torchrun ... bench.py ...`."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world != args.gpus:
+        # the job must have exactly --gpus ranks: a silent 1-rank run of `--gpus 8` would
+        # report a 1-GPU number as an 8-GPU one
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} "
+                         "ranks")
     if world > 1 and args.impl == "reference":
         return world, rank, local  # rank 0 runs the CPU oracle, the others exit; no process group
     if world > 1:
         import torch.distributed as dist
+        if args.impl == "ours" and args.backend == "nccl" and torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, "
+                             f"{torch.cuda.device_count()} visible")
         if args.impl == "ours":
             # one rank per GPU; with fewer GPUs than ranks (gloo test mode) ranks share devices
             torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
@@ -254,7 +280,7 @@ def run_reference(args, world, rank):
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} steps x {cores} whole heads of {cfg.name}"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": 0}
+            "gpu_launches": 0, "world_size": world}
     print(json.dumps(line), flush=True)
 
 
@@ -527,6 +553,10 @@ def bench_gemm(name, pk, iters=10):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":

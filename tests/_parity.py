@@ -100,6 +100,26 @@ def check_against_oracle(q, k, v, causal, scale, rows_per_head=None, heads=None,
     return stats, (o, lse)
 
 
+def compare_outputs_with_oracle(q, k, v, o, lse, causal, scale, rows_per_head, label=""):
+    """Compare GIVEN outputs o[B,Sq,Hq,D] / lse[B,Hq,Sq] (any producer: e.g. a replicated
+    output written by several ranks' epilogues) with the fp64 oracle on ``rows_per_head``
+    rows of EVERY (b, h), computed from the same q/k/v."""
+    B, Sq, Hq, D = q.shape
+    qb, kb, vb = to_bits(q), to_bits(k), to_bits(v)
+    work = [(b, h, rows_per_head) for b in range(B) for h in range(Hq)]
+    res = oracle.attn_rows_parallel(qb, kb, vb, odt(q.dtype), int(causal), scale, work)
+    bi = torch.tensor([b for (b, h, rows) in work for _ in rows], device=o.device)
+    hi = torch.tensor([h for (b, h, rows) in work for _ in rows], device=o.device)
+    ri = torch.tensor([r for (b, h, rows) in work for r in rows], device=o.device)
+    og = o[bi, ri, hi, :].double().cpu().numpy()
+    lg = None if lse is None else lse[bi, hi, ri].double().cpu().numpy()
+    orf = np.concatenate([r[0] for r in res])
+    lrf = np.concatenate([r[1] for r in res])
+    stats = compare(og, lg, orf, lrf, label)
+    stats["rows_checked"] = int(og.shape[0])
+    return stats
+
+
 def gen(B, Hq, Hkv, Sq, Skv, D, dtype, seed):
     return gen_qkv(B, Hq, Hkv, Sq, Skv, D, dtype, seed, "cuda")
 

@@ -37,3 +37,35 @@ def test_our_arm_fails_loudly_without_a_gpu():
              "--e2e-steps", "0"])
     assert r.returncode != 0
     assert '"value"' not in r.stdout
+
+
+def test_gpus_n_starts_n_ranks_itself():
+    """`bench.py --gpus 2` with no launcher environment starts the 2 ranks itself (the
+    driver's torchrun form); the reference arm's line comes from rank 0 of a world of 2."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                        "reference", "--steps", "1", "--warmup", "0", "--workload", "C1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["world_size"] == 2 and line["impl"] == "reference"
+
+
+def test_mismatched_world_is_rejected():
+    """A launcher world that differs from --gpus exits non-zero instead of reporting a
+    number for the wrong GPU count."""
+    env = {**os.environ, "WORLD_SIZE": "3", "RANK": "0", "LOCAL_RANK": "0"}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                        "reference", "--steps", "1", "--warmup", "0", "--workload", "C1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0
+    assert "WORLD_SIZE=3" in r.stderr
+    assert '"value"' not in r.stdout
+    env1 = {**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"}
+    r1 = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--impl",
+                         "reference", "--steps", "1", "--warmup", "0", "--workload", "C1"],
+                        cwd=ROOT, capture_output=True, text=True, timeout=300, env=env1)
+    assert r1.returncode != 0 and '"value"' not in r1.stdout

@@ -224,3 +224,33 @@ def test_rejects_bad_arguments():
     q, qp, kv, kp = mla_inputs(1, 2, 1, 4, 8, 4, tdt, 1)
     with pytest.raises(ValueError):
         oracle.mla_decode(q, qp, kv, kp, 1, 0.1, np.array([5], np.int32))  # n_b > Skv
+
+
+@pytest.mark.parametrize("ragged", [True, False])
+def test_parallel_helper_equals_whole_batch_oracle(ragged):
+    """oracle.mla_decode_parallel (per-batch slices on host threads; it produces every MLA
+    GPU expected value) must equal the whole-batch oracle.mla_decode exactly — including
+    the per-batch seqlens slice (a mis-sliced length or batch index changes the result) —
+    for any batch subset in any order, and its batch-0 row must equal the independent
+    explicit-matrix form (oracle.mla_brute)."""
+    B, H, Hkv, Skv, Dl, Dr = 6, 8, 2, 70, 32, 16
+    q, qp, kv, kp = mla_inputs(B, H, Hkv, Skv, Dl, Dr, torch.bfloat16, 31)
+    sl = gen_seqlens(B, Skv, 31, lo=0) if ragged else None
+    if ragged:
+        sl[3] = 0  # an empty cache among the requested batches
+        sl[1] = Skv
+    scale = 0.17
+    o_all, l_all = oracle.mla_decode(q, qp, kv, kp, oracle.ORACLE_BF16, scale, sl)
+    subset = [5, 0, 3, 1] if ragged else [2, 4]
+    got = oracle.mla_decode_parallel(q, qp, kv, kp, oracle.ORACLE_BF16, scale, sl, batches=subset,
+                                     threads=3)
+    assert sorted(got) == sorted(subset)
+    for b in subset:
+        o_b, l_b = got[b]
+        assert np.array_equal(o_b, o_all[b]), b
+        assert np.array_equal(l_b, l_all[b]), b
+    if ragged:
+        assert np.all(got[3][0] == 0.0) and np.all(np.isneginf(got[3][1]))
+    _, _, o_bf, l_bf = oracle.mla_brute(q, qp, kv, kp, oracle.ORACLE_BF16, scale, subset[1], sl)
+    np.testing.assert_allclose(got[subset[1]][0], o_bf, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(got[subset[1]][1], l_bf, rtol=0, atol=1e-12)
