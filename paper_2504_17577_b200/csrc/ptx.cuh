@@ -378,6 +378,18 @@ __device__ __forceinline__ void mma_f16_ss_2sm(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// M=256 MMA over the CTA pair with A read from TENSOR memory ("TS" form): each CTA's TMEM
+// holds its 128 rows of A at `tmem_a` (K-major, two 16-bit elements per 32-bit column);
+// B from shared memory split across the pair as in mma_f16_ss_2sm. Leader only.
+__device__ __forceinline__ void mma_f16_ts_2sm(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // commit: arrive once on `bar` (same smem offset) in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_2sm(uint32_t bar) {
   asm volatile(
@@ -393,6 +405,20 @@ __device__ __forceinline__ void clc_try_cancel_multicast(uint32_t resp_smem, uin
       "cluster::all.b128 [%0], [%1];" ::"r"(resp_smem),
       "r"(bar)
       : "memory");
+}
+
+// One lane of the (fully converged) warp returns true. MMA issuers run their control flow
+// on the whole warp and issue tcgen05 ops under elect_one(), so descriptor arithmetic stays
+// warp-uniform (uniform registers) instead of a per-thread R2UR "waterfall" around every
+// UTCHMMA (measured: single-lane issue ~2x slower per MMA).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 // ------------------------------------------------------------------ named barriers
