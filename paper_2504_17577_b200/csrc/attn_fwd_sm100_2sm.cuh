@@ -216,8 +216,10 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
       __syncwarp();
     } else if ((warp == 1 || warp == 2) && leader) {
       // =========== MMA issuers (leader only): warp 1 -> tile 0, warp 2 -> tile 1 ===========
+      // whole warp: uniform control flow, tcgen05 ops by one elected lane (elect_one():
+      // descriptors stay in uniform registers, no per-MMA R2UR waterfall)
       const int t = warp - 1;
-      if (lane == 0) {
+      {
         constexpr uint32_t FMT = BF16 ? 1u : 0u;
         // S = Q K^T over the pair: M=256 (rows split), N=128 keys (B split 64/64)
         const uint32_t IDESC_QK = make_idesc_f16(FMT, 2 * BM, BN, 0, 0, p.neg ? 1u : 0u);
@@ -239,38 +241,38 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
           auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
           mbar_wait(bar_q_full, k & 1);
-          TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 7);  // Q ready (unit start)
+          if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 7);  // Q ready (unit start)
           auto issue_s = [&](int j) {
             const int sl = kpos(j) % C::NST;
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 0);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 0);
             mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 1);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 1);
 #ifndef TLATTN_MMA_ONLY
             if (cs > 0) mbar_wait(bar_s_free(t), (cs - 1) & 1);  // both CTAs read S_t
 #endif
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 2);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 2);
             tc_fence_after();
             const uint32_t kb = sKV + sl * C::SLOT_BYTES;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
-              mma_f16_ss_2sm(tm_s,
+              if (elect_one()) mma_f16_ss_2sm(tm_s,
                              make_sdesc_sw128(qa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024),
                              make_sdesc_sw128(kb + (kk >> 2) * C::K_HALF_CHUNK + (kk & 3) * 32, 16, 1024),
                              IDESC_QK, kk > 0 ? 1u : 0u);
             }
-            mma_commit_2sm(bar_s_full(t));
-            mma_commit_2sm(bar_kv_empty(sl));
+            if (elect_one()) mma_commit_2sm(bar_s_full(t));
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
             ++cs;
           };
           auto issue_pv = [&](int j) {
             const int sl = vpos(j) % C::NST;
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 3);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 3);
             mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 4);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 4);
 #ifndef TLATTN_MMA_ONLY
             mbar_wait(bar_p_full(t), cpv & 1);  // P_t written in both CTAs
 #endif
-            TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 5);
+            if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * (j & 15) + 5);
             tc_fence_after();
             const uint32_t vb = sKV + sl * C::SLOT_BYTES;
 #pragma unroll
@@ -281,40 +283,40 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
                 tc_fence_after();
               }
 #endif
-              mma_f16_ss_2sm(tm_o,
+              if (elect_one()) mma_f16_ss_2sm(tm_o,
                              make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024),
                              make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024), IDESC_PV,
                              (j > 0 || kk > 0) ? 1u : 0u);
             }
-            mma_commit_2sm(bar_o_done(t));
-            mma_commit_2sm(bar_kv_empty(sl));
+            if (elect_one()) mma_commit_2sm(bar_o_done(t));
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
             ++cpv;
           };
           if (nt > 0) {
             issue_s(0);
-            if (nt == 1) mma_commit_2sm(bar_q_empty);
+            if (nt == 1 && elect_one()) mma_commit_2sm(bar_q_empty);
             for (int j = 0; j < nt; ++j) {
               if (j + 1 < nt) {
                 issue_s(j + 1);
-                if (j + 2 == nt) mma_commit_2sm(bar_q_empty);
+                if (j + 2 == nt && elect_one()) mma_commit_2sm(bar_q_empty);
               }
               issue_pv(j);
             }
           } else {
-            mma_commit_2sm(bar_q_empty);
+            if (elect_one()) mma_commit_2sm(bar_q_empty);
           }
           for (int j = nt; j < nmax; ++j) {  // blocks only the other tile needs
             int sl = kpos(j) % C::NST;
             mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
-            mma_commit_2sm(bar_kv_empty(sl));
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
             sl = vpos(j) % C::NST;
             mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
-            mma_commit_2sm(bar_kv_empty(sl));
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
           }
-          TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 6);  // issuer done with the unit's MMAs
+          if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 6);  // issuer done with the unit's MMAs
           mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
           const int nxt = clc_query(sSched + 16 * (k & 1));
-          mbar_arrive(bar_sched_empty(k & 1));
+          if (elect_one()) mbar_arrive(bar_sched_empty(k & 1));
           if (nxt < 0) break;
           unit = nxt >> 1;
         }

@@ -34,7 +34,7 @@ struct DeviceInfo {
   int major = 0, minor = 0;
   bool ok = false;
   // per kernel instantiation: cudaFuncAttributeMaxDynamicSharedMemorySize already set.
-  // Slots: attention 0-5, replicated-output attention 8-13, GEMM 16-17.
+  // Slots: attention 0-7, replicated-output attention 8-15, GEMM 16-17.
   bool smem_set[32] = {};
 };
 
@@ -180,11 +180,14 @@ int launch_2sm(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
 }
 
 // Kernel selection: D=128 runs on CTA pairs (2-SM tcgen05), D=64 on single CTAs.
-// TLATTN_KERNEL=1cta forces the single-CTA kernel for D=128 (A/B comparisons only).
+// TLATTN_KERNEL=1cta forces the single-CTA kernel for D=128 (A/B comparisons only; read
+// once per process).
 bool use_2sm(int D) {
-  if (D != 128) return false;
-  const char* e = std::getenv("TLATTN_KERNEL");
-  return !(e && std::strcmp(e, "1cta") == 0);
+  static const bool force_1cta = [] {
+    const char* e = std::getenv("TLATTN_KERNEL");
+    return e && std::strcmp(e, "1cta") == 0;
+  }();
+  return D == 128 && !force_1cta;
 }
 
 template <int D, bool BF16, class PT>

@@ -9,7 +9,7 @@
 using namespace tlattn;
 
 template <int NC, int EMU, int MODE>
-__global__ void kern(float* out, int iters, long long* clk) {
+__global__ void __launch_bounds__(256, 1) kern(float* out, int iters, long long* clk) {
   float s[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) s[i] = 0.01f * ((threadIdx.x * 7 + i * 13) % 97) - 0.5f;
@@ -22,7 +22,8 @@ __global__ void kern(float* out, int iters, long long* clk) {
 #pragma unroll
     for (int i = 0; i < NC; ++i) sl[i] = s[i] + 1e-7f * it;  // fresh "S" every block
     float mx = 0.f;
-    if (MODE != 2) mx = mask_max_cols<0, NC>(sl, 0, 1 << 30, false);
+    if (MODE == 3) mx = mask_max_cols<0, NC>(sl, 0, (threadIdx.x & 127) * NC / 128, true);  // diagonal block
+    else if (MODE != 2) mx = mask_max_cols<0, NC>(sl, 0, 1 << 30, false);
     float m_new, alpha, m_use;
     row_max_finish(mx, 1.4426950408889634f * 0.0883883f, m, m_new, alpha, m_use);
     uint64_t acc[4];
@@ -62,6 +63,8 @@ void run(const char* name, int warps) {
 
 int main() {
   run<64, 0, 0>("64col emu0", 8);
+  run<128, 0, 3>("128col emu0 masked (2 tiles)", 8);
+  run<128, 0, 0>("128col emu0 unmasked (2 tiles)", 8);
   run<64, 1, 0>("64col emu1", 8);
   run<64, 2, 0>("64col emu2", 8);
   run<64, 3, 0>("64col emu3", 8);
@@ -69,7 +72,10 @@ int main() {
   run<128, 0, 0>("128col emu0", 4);
   run<128, 2, 0>("128col emu2", 4);
   run<128, 0, 0>("128col emu0 (2 tiles)", 8);
-  run<64, 2, 0>("64col emu2 16w", 16);
+  run<64, 2, 0>("64col emu2 16w (2 tiles)", 16);
+  run<64, 0, 0>("64col emu0 16w (2 tiles)", 16);
+  run<64, 3, 0>("64col emu3 16w (2 tiles)", 16);
+  run<64, 2, 0>("64col emu2 20w", 20);
   run<32, 2, 0>("32col emu2 16w", 16);
   return 0;
 }
