@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TLATTN_VERSION 0x000200 /* 0.2.0: + tl_attn_fwd_replicated, tl_peer_barrier, tl_ipc_*; tl_gemm M = 1 path */
+#define TLATTN_VERSION 0x000300 /* 0.3.0: bounded tl_peer_barrier (+ _set_timeout_ns, _check); tl_attn_set/get_option */
 
 enum tl_dtype { TL_DTYPE_F16 = 0, TL_DTYPE_BF16 = 1 };
 
@@ -56,7 +56,10 @@ enum tl_status {
      aligned; a tensor too large for 32-bit TMA coordinates; device not sm_100 */
   TL_ERR_UNSUPPORTED = 2,
   /* a CUDA runtime / driver call failed (no device, tensor-map encode, launch) */
-  TL_ERR_CUDA = 3
+  TL_ERR_CUDA = 3,
+  /* tl_peer_barrier: a peer did not arrive within the barrier's timeout (reported by
+     tl_peer_barrier_check after the barrier kernel ran) */
+  TL_ERR_TIMEOUT = 4
 };
 
 /*
@@ -203,18 +206,31 @@ int tl_attn_fwd_replicated(const void* q, const void* k, const void* v,
  * tl_peer_barrier — stream-ordered device-side barrier among `world` ranks (one kernel).
  *
  *   flags   HOST array of `world` device pointers (world <= 8): flags[r] = rank r's array
- *           of `world` uint32 counters as mapped in THIS process (flags[rank] = own array;
- *           peers' opened with tl_ipc_open_handle); zero-initialised once by their owners
+ *           of TL_PEER_FLAG_WORDS uint32 as mapped in THIS process (flags[rank] = own array;
+ *           peers' opened with tl_ipc_open_handle); zero-initialised once by their owners.
+ *           Words [0, world) are the epoch counters, word TL_PEER_STATUS_WORD the status.
  *   rank    this rank; epoch: a value that increases by 1 on every use (wraps mod 2^32)
  *
  * Rank `rank` stores `epoch` into flags[r][rank] for every r (system-scope release, after
  * this stream's earlier work) and waits until flags[rank][r] >= epoch for every r
  * (acquire). After it, this stream sees every rank's writes issued before that rank's
  * barrier (e.g. tl_attn_fwd_replicated into this rank's output). All ranks must call it
- * with the same epoch sequence, otherwise it waits forever.
- * Errors: TL_ERR_INVALID_VALUE (NULL / misaligned flags, bad world / rank), TL_ERR_CUDA.
+ * with the same epoch sequence.
+ * The wait is BOUNDED: a peer that has not arrived after the timeout (default 10 s,
+ * tl_peer_barrier_set_timeout_ns) makes the kernel store TL_ERR_TIMEOUT into
+ * flags[rank][TL_PEER_STATUS_WORD] and return instead of hanging the stream; read it with
+ * tl_peer_barrier_check. The status word is sticky until the owner rewrites it.
+ * Errors (synchronous): TL_ERR_INVALID_VALUE (NULL / misaligned flags, bad world / rank),
+ * TL_ERR_CUDA.
  */
+#define TL_PEER_FLAG_WORDS 16
+#define TL_PEER_STATUS_WORD 15
 int tl_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream);
+/* Timeout of later tl_peer_barrier calls on this host thread, in nanoseconds (> 0). */
+int tl_peer_barrier_set_timeout_ns(uint64_t ns);
+/* Synchronises the current device, then reads own_flags[TL_PEER_STATUS_WORD]: TL_OK, or
+ * TL_ERR_TIMEOUT if a barrier on this rank's flags timed out; TL_ERR_CUDA / _INVALID_VALUE. */
+int tl_peer_barrier_check(const uint32_t* own_flags);
 
 /* CUDA IPC helpers for the peer buffers above (wrappers over cudaIpc*MemHandle): a handle
  * is tl_ipc_handle_bytes() opaque bytes the caller ships to other processes (e.g. with
@@ -232,6 +248,32 @@ const char* tl_attn_strerror(int status);
 
 /* TLATTN_VERSION of the loaded library. */
 int tl_attn_version(void);
+
+/*
+ * Experiment / test options (process-wide; NOT needed for normal use). Each defaults to
+ * -1 = automatic (the launcher's measured choice); the tools/ A/B scripts seed them once
+ * from the environment (TLATTN_KERNEL=1cta, TLATTN_UNIT_TILES, TLATTN_LPT, TLATTN_GEMV_TC,
+ * TLATTN_MLA_HC, TLATTN_MLA_CL) on first use. Values outside an option's set are ignored
+ * by the launcher (automatic). tl_attn_set_option returns TL_OK or TL_ERR_INVALID_VALUE
+ * (unknown option); tl_attn_get_option returns the current value (-2: unknown option).
+ *   TL_OPT_FORCE_1CTA  1: D = 128 on the single-CTA kernel instead of CTA pairs
+ *   TL_OPT_UNIT_TILES  1 or 2 query tiles of 256 rows per CTA-pair unit
+ *   TL_OPT_LPT         0: (b, h)-major unit order; 1: heaviest query block first (LPT)
+ *   TL_OPT_GEMV_TC     GEMV (M = 1) column tile: 32, 64, 128 or 256
+ *   TL_OPT_MLA_HC      MLA heads per CTA tile: 32 or 64
+ *   TL_OPT_MLA_CL      MLA K/V multicast cluster size: 1, 2 or 4
+ */
+enum tl_option {
+  TL_OPT_FORCE_1CTA = 0,
+  TL_OPT_UNIT_TILES = 1,
+  TL_OPT_LPT = 2,
+  TL_OPT_GEMV_TC = 3,
+  TL_OPT_MLA_HC = 4,
+  TL_OPT_MLA_CL = 5,
+  TL_OPT_COUNT = 6
+};
+int tl_attn_set_option(int option, int value);
+int tl_attn_get_option(int option);
 
 /* Number of kernel launches the most recent successful tl_attn_fwd / tl_attn_fwd_host /
  * tl_attn_fwd_replicated / tl_peer_barrier / tl_gemm / tl_mla_decode call on this host

@@ -29,6 +29,9 @@ from .tlattn import (  # noqa: F401
     tl_attn_version,
     tl_attn_fwd_replicated,
     tl_peer_barrier,
+    tl_peer_barrier_set_timeout_ns,
+    tl_peer_barrier_check,
+    TL_ERR_TIMEOUT,
     tl_ipc_get_handle,
     tl_ipc_open_handle,
     tl_ipc_close_handle,

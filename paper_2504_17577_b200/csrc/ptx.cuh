@@ -77,25 +77,37 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
-// Blocking wait on phase `parity`. Watchdog: a wait that has not completed after
-// TLATTN_WATCHDOG_NS of wall time traps instead of hanging the GPU (a phase bug must
-// fail fast).
+// Blocking wait on phase `parity`. Watchdog (debug builds, or -DTLATTN_WATCHDOG_NS=<ns>):
+// a wait that has not completed after TLATTN_WATCHDOG_NS of wall time reports (TLATTN_DBG)
+// or traps instead of hanging the GPU, so a phase bug fails fast during development
+// (SURVEY §5). Release builds have no watchdog: a healthy kernel that is preempted,
+// time-sliced (MPS, two processes on one GPU) or run under a debugger / compute-sanitizer
+// may legitimately wait for seconds, and a trap would destroy the caller's CUDA context.
 #ifndef TLATTN_WATCHDOG_NS
+#ifdef TLATTN_DBG
 #define TLATTN_WATCHDOG_NS 4000000000ull
+#else
+#define TLATTN_WATCHDOG_NS 0ull
+#endif
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer();
-  uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS) {
+  if constexpr (TLATTN_WATCHDOG_NS == 0) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+  } else {
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+      if ((++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS) {
 #ifdef TLATTN_DBG
-      printf("watchdog: block %d thread %d barrier smem 0x%x parity %u\n", blockIdx.x, threadIdx.x,
-             bar, parity);
-      return;
+        printf("watchdog: block %d thread %d barrier smem 0x%x parity %u\n", blockIdx.x,
+               threadIdx.x, bar, parity);
+        return;
 #else
-      __trap();
+        __trap();
 #endif
+      }
     }
   }
 }
@@ -323,7 +335,8 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
   const uint64_t t0 = globaltimer();
   uint32_t n = 0;
   while (!mbar_try_wait_cluster(bar, parity)) {
-    if ((++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS) __trap();
+    if (TLATTN_WATCHDOG_NS != 0 && (++n & 1023u) == 0 && globaltimer() - t0 > TLATTN_WATCHDOG_NS)
+      __trap();
   }
 }
 // 2-SM TMA load: data into this CTA's smem, transaction bytes counted on `bar_cluster`

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "../../include/tlattn.h"
@@ -28,6 +29,33 @@ namespace {
 
 thread_local int g_last_launches = 0;
 unsigned long long* g_trace = nullptr;  // debug builds only (tl_attn_debug_trace)
+
+// A/B experiment options (include/tlattn.h tl_attn_set_option): process-wide atomics, set
+// once from the environment on first use (TLATTN_KERNEL=1cta, TLATTN_UNIT_TILES, TLATTN_LPT,
+// TLATTN_GEMV_TC, TLATTN_MLA_HC, TLATTN_MLA_CL — for the tools/ A/B scripts) and changed only
+// through tl_attn_set_option, so production calls do no getenv. -1 = automatic.
+std::atomic<int> g_opt[TL_OPT_COUNT];
+std::once_flag g_opt_once;
+void init_options() {
+  std::call_once(g_opt_once, [] {
+    auto env = [](const char* name) {
+      const char* e = std::getenv(name);
+      return e ? std::atoi(e) : -1;
+    };
+    const char* k = std::getenv("TLATTN_KERNEL");
+    g_opt[TL_OPT_FORCE_1CTA] = (k && std::strcmp(k, "1cta") == 0) ? 1 : -1;
+    g_opt[TL_OPT_UNIT_TILES] = env("TLATTN_UNIT_TILES");
+    g_opt[TL_OPT_LPT] = env("TLATTN_LPT");
+    g_opt[TL_OPT_GEMV_TC] = env("TLATTN_GEMV_TC");
+    g_opt[TL_OPT_MLA_HC] = env("TLATTN_MLA_HC");
+    g_opt[TL_OPT_MLA_CL] = env("TLATTN_MLA_CL");
+  });
+}
+int opt(int o) {
+  init_options();
+  return g_opt[o].load(std::memory_order_relaxed);
+}
+
 
 struct DeviceInfo {
   int sm_count = 0;
@@ -180,15 +208,8 @@ int launch_2sm(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
 }
 
 // Kernel selection: D=128 runs on CTA pairs (2-SM tcgen05), D=64 on single CTAs.
-// TLATTN_KERNEL=1cta forces the single-CTA kernel for D=128 (A/B comparisons only; read
-// once per process).
-bool use_2sm(int D) {
-  static const bool force_1cta = [] {
-    const char* e = std::getenv("TLATTN_KERNEL");
-    return e && std::strcmp(e, "1cta") == 0;
-  }();
-  return D == 128 && !force_1cta;
-}
+// TL_OPT_FORCE_1CTA = 1 forces the single-CTA kernel for D=128 (A/B comparisons only).
+bool use_2sm(int D) { return D == 128 && opt(TL_OPT_FORCE_1CTA) != 1; }
 
 template <int D, bool BF16, class PT>
 int launch(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
@@ -254,10 +275,7 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
   if (pair) {
     const long long units512 = (long long)B * Hq * ((Sq + 511) / 512);
     if (2 * units512 <= di->sm_count / 2) prm.unit_tiles = 1;
-    if (const char* e = std::getenv("TLATTN_UNIT_TILES")) {  // A/B experiments only
-      const int v = std::atoi(e);
-      if (v == 1 || v == 2) prm.unit_tiles = v;
-    }
+    if (const int v = opt(TL_OPT_UNIT_TILES); v == 1 || v == 2) prm.unit_tiles = v;
   }
   const int unit_rows = pair ? 2 * BM * prm.unit_tiles : TILES * BM;
   prm.n_mblk = (Sq + unit_rows - 1) / unit_rows;
@@ -276,11 +294,11 @@ int run_attn(PT& prm, const void* q, const void* k, const void* v, int B, int Hq
   const double heaviest = tiles_per_unit * nb;                 // tile-blocks of the top unit
   const double share = (double)B * Hq * std::ceil(Sq / tile_rows) * nb * 0.5 / workers;
   prm.lpt = (causal && (kv_bytes <= 64.0 * (1 << 20) || heaviest >= 0.05 * share)) ? 1 : 0;
-  if (const char* e = std::getenv("TLATTN_LPT")) {  // A/B experiments only
-    const int v = std::atoi(e);
-    if (v == 0 || v == 1) prm.lpt = v;
-  }
-  prm.n_units = B * Hq * prm.n_mblk;  // bounded in validate()
+  if (const int v = opt(TL_OPT_LPT); v == 0 || v == 1) prm.lpt = v;
+  // grid bound re-checked after the unit-size choice (validate() bounded the default)
+  const long long n_units = (long long)B * Hq * prm.n_mblk;
+  if ((pair ? 2 : 1) * n_units > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
+  prm.n_units = static_cast<int>(n_units);
   prm.fd_mblk = make_fastdiv(prm.n_mblk);
   prm.fd_nbh = make_fastdiv(B * Hq);
   prm.fd_hq = make_fastdiv(Hq);
@@ -359,20 +377,30 @@ namespace {
 struct PeerFlags {
   uint32_t* ptr[kMaxOuts];
 };
+thread_local uint64_t g_peer_timeout_ns = 10000000000ull;  // 10 s
 // One block, `world` threads: thread i publishes `epoch` into rank i's flag slot [rank]
 // (system-scope release: this rank's earlier writes into rank i's memory — the replicated
 // O / LSE of the previous kernels on this stream — are visible before the flag), then
-// waits until its own slot [i] holds >= epoch (acquire: rank i's writes are visible).
-__global__ void tl_peer_barrier_kernel_v(const PeerFlags f, int world, int rank, uint32_t epoch) {
+// waits until its own slot [i] holds >= epoch (acquire: rank i's writes are visible). The
+// wait is bounded: after timeout_ns the thread records TL_ERR_TIMEOUT in this rank's
+// status word and returns (a dead peer must not hang the stream forever).
+__global__ void tl_peer_barrier_kernel_v(const PeerFlags f, int world, int rank, uint32_t epoch,
+                                         uint64_t timeout_ns) {
   const int i = threadIdx.x;
   if (i >= world) return;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.ptr[i] + rank), "r"(epoch) : "memory");
   const uint32_t* mine = f.ptr[rank] + i;
+  const uint64_t t0 = globaltimer();
   uint32_t v;
-  do {
+  for (uint32_t n = 0;; ++n) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
-  } while ((int32_t)(v - epoch) < 0);
+    if ((int32_t)(v - epoch) >= 0) break;
+    if ((n & 255u) == 255u && globaltimer() - t0 > timeout_ns) {
+      atomicExch(f.ptr[rank] + TL_PEER_STATUS_WORD, (uint32_t)TL_ERR_TIMEOUT);
+      break;
+    }
+  }
 }
 }  // namespace
 
@@ -391,10 +419,29 @@ extern "C" int tl_peer_barrier(uint32_t* const* flags, int world, int rank, uint
   DeviceInfo* di;
   int rc;
   if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
-  tl_peer_barrier_kernel_v<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(f, world, rank, epoch);
+  tl_peer_barrier_kernel_v<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      f, world, rank, epoch, g_peer_timeout_ns);
   if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
   g_last_launches = 1;
   return TL_OK;
+}
+
+extern "C" int tl_peer_barrier_set_timeout_ns(uint64_t ns) {
+  if (ns == 0) return TL_ERR_INVALID_VALUE;
+  g_peer_timeout_ns = ns;
+  return TL_OK;
+}
+
+extern "C" int tl_peer_barrier_check(const uint32_t* own_flags) {
+  if (!own_flags || reinterpret_cast<uintptr_t>(own_flags) % 4 != 0) return TL_ERR_INVALID_VALUE;
+  uint32_t status = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(&status, own_flags + TL_PEER_STATUS_WORD, sizeof status, cudaMemcpyDeviceToHost) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
+  return status == 0 ? TL_OK : (int)status;
 }
 
 // Handle blob = cudaIpcMemHandle_t of the allocation + the byte offset of dev_ptr inside it
@@ -531,11 +578,22 @@ extern "C" int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_
     d2h = g_copy_streams[dev][1];
   }
   const int nchunks = (B + pl.cb - 1) / pl.cb;
-  cudaEvent_t ev_start, ev_in[2], ev_comp[2], ev_out[2];
-  auto mk = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
-  if (!mk(&ev_start)) return TL_ERR_CUDA;
-  for (int i = 0; i < 2; ++i)
-    if (!mk(&ev_in[i]) || !mk(&ev_comp[i]) || !mk(&ev_out[i])) return TL_ERR_CUDA;
+  // events: [0] start, [1..2] in, [3..4] comp, [5..6] out, [7..8] tails of the copy streams.
+  // Every created event is destroyed on every exit path.
+  cudaEvent_t evs[9] = {};
+  int n_ev = 0;
+  auto destroy_events = [&] {
+    for (int i = 0; i < n_ev; ++i) cudaEventDestroy(evs[i]);
+  };
+  for (; n_ev < 9; ++n_ev) {
+    if (cudaEventCreateWithFlags(&evs[n_ev], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      destroy_events();
+      return TL_ERR_CUDA;
+    }
+  }
+  cudaEvent_t ev_start = evs[0], ev_in[2] = {evs[1], evs[2]}, ev_comp[2] = {evs[3], evs[4]},
+              ev_out[2] = {evs[5], evs[6]};
   bool ok = cudaEventRecord(ev_start, cs) == cudaSuccess;
   ok = ok && cudaStreamWaitEvent(h2d, ev_start, 0) == cudaSuccess;
   int launches = 0;
@@ -567,14 +625,15 @@ extern "C" int tl_attn_fwd_host(const void* q_h, const void* k_h, const void* v_
       ok = ok && cudaMemcpyAsync((uint8_t*)lse_h + (size_t)b0 * pl.lse_b, dlse, nb * pl.lse_b, cudaMemcpyDeviceToHost, d2h) == cudaSuccess;
     ok = ok && cudaEventRecord(ev_out[s], d2h) == cudaSuccess;
   }
-  // caller's stream resumes after the last device->host copy
-  if (ok && rc == TL_OK) ok = cudaStreamWaitEvent(cs, ev_out[(nchunks - 1) & 1], 0) == cudaSuccess;
-  cudaEventDestroy(ev_start);
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(ev_in[i]);
-    cudaEventDestroy(ev_comp[i]);
-    cudaEventDestroy(ev_out[i]);
-  }
+  // The caller's stream resumes after EVERY copy queued on the two copy streams — on the
+  // error paths too, so the caller may free or reuse ws and the host buffers once its
+  // stream is done.
+  const bool tails = cudaEventRecord(evs[7], h2d) == cudaSuccess &&
+                     cudaEventRecord(evs[8], d2h) == cudaSuccess &&
+                     cudaStreamWaitEvent(cs, evs[7], 0) == cudaSuccess &&
+                     cudaStreamWaitEvent(cs, evs[8], 0) == cudaSuccess;
+  ok = ok && tails;
+  destroy_events();
   if (rc != TL_OK) return rc;
   if (!ok) {
     cudaGetLastError();
@@ -639,10 +698,7 @@ extern "C" int tl_gemm(const void* a, const void* b, void* c, int M, int N, int 
     gp.K = K;
     int tc = N >= 32768 ? 128 : 256;  // measured: 128 is 4-5 % faster for N >= 32768
     while (tc > 32 && (N + tc - 1) / tc < 18) tc /= 2;
-    if (const char* e = std::getenv("TLATTN_GEMV_TC")) {  // A/B experiments only
-      const int v = std::atoi(e);
-      if (v == 32 || v == 64 || v == 128 || v == 256) tc = v;
-    }
+    if (const int v = opt(TL_OPT_GEMV_TC); v == 32 || v == 64 || v == 128 || v == 256) tc = v;
     gp.tc = tc;
     const long long tiles = (N + tc - 1) / tc;
     if (tiles > 0x7fffffffLL) return TL_ERR_UNSUPPORTED;
@@ -682,10 +738,7 @@ struct MlaPlan {
 };
 
 int mla_cluster_size(int T) {
-  if (const char* e = std::getenv("TLATTN_MLA_CL")) {  // A/B experiments only
-    const int v = std::atoi(e);
-    if ((v == 1 || v == 2 || v == 4) && T % v == 0) return v;
-  }
+  if (const int v = opt(TL_OPT_MLA_CL); (v == 1 || v == 2 || v == 4) && T % v == 0) return v;
   // measured on B200: multicast clusters ran slower than independent CTAs
   // (lockstep ring, no L2 relief at cluster size <= 4), so the default is 1
   (void)T;
@@ -700,10 +753,7 @@ MlaPlan plan_mla(int B, int H, int Hkv, int dev, int sm_count) {
   const int g = H / Hkv;
   // 64-head tiles read the latent cache half as often as 32-head tiles
   pl.HC = g >= 64 ? 64 : 32;
-  if (const char* e = std::getenv("TLATTN_MLA_HC")) {  // A/B experiments only
-    const int v = std::atoi(e);
-    if (v == 32 || v == 64) pl.HC = v;
-  }
+  if (const int v = opt(TL_OPT_MLA_HC); v == 32 || v == 64) pl.HC = v;
   pl.T = (g + pl.HC - 1) / pl.HC;
   pl.NHG = Hkv * pl.T;
   pl.CL = mla_cluster_size(pl.T);
@@ -877,11 +927,24 @@ extern "C" const char* tl_attn_strerror(int status) {
     case TL_ERR_INVALID_VALUE: return "TL_ERR_INVALID_VALUE: invalid argument (null pointer, size < 1, causal not 0/1, non-finite scale, unknown dtype, or workspace too small)";
     case TL_ERR_UNSUPPORTED: return "TL_ERR_UNSUPPORTED: unsupported configuration (D not 64/128, Hq % Hkv != 0, misaligned pointer, size limit, or device is not sm_100)";
     case TL_ERR_CUDA: return "TL_ERR_CUDA: a CUDA runtime/driver call failed";
+    case TL_ERR_TIMEOUT: return "TL_ERR_TIMEOUT: a peer did not reach the device barrier before its timeout";
     default: return "unknown tl_status code";
   }
 }
 
 extern "C" int tl_attn_version(void) { return TLATTN_VERSION; }
+
+extern "C" int tl_attn_set_option(int option, int value) {
+  if (option < 0 || option >= TL_OPT_COUNT) return TL_ERR_INVALID_VALUE;
+  init_options();
+  g_opt[option].store(value < 0 ? -1 : value, std::memory_order_relaxed);
+  return TL_OK;
+}
+
+extern "C" int tl_attn_get_option(int option) {
+  if (option < 0 || option >= TL_OPT_COUNT) return -2;
+  return opt(option);
+}
 
 // Debug hook (not part of include/tlattn.h): device buffer of >= 8000 u64 that receives
 // clock64 pipeline events of CTA 0 in builds compiled with -DTLATTN_TRACE.

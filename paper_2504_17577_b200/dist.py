@@ -117,7 +117,7 @@ class ReplicatedOutput:
         lse_bytes = B * Hq * Sq * 4 if with_lse else 0
         self.off_lse = _al(o_bytes)
         self.off_flags = self.off_lse + _al(lse_bytes)
-        total = self.off_flags + _al(4 * 8)
+        total = self.off_flags + _al(4 * T.TL_PEER_FLAG_WORDS)
         self.buf = torch.zeros(total, dtype=torch.uint8, device=dev)
         self.o = self.buf[:o_bytes].view(dtype).view(B, Sq, Hq, D)
         self.lse = (self.buf[self.off_lse:self.off_lse + lse_bytes].view(torch.float32)
@@ -146,14 +146,37 @@ class ReplicatedOutput:
         self.epoch += 1
         T.tl_peer_barrier(self.flag_ptrs, self.shard.rank, self.epoch, stream)
 
+    def check(self):
+        """Synchronise and raise TlAttnError(TL_ERR_TIMEOUT) if one of this rank's device
+        barriers gave up waiting for a peer (a dead rank no longer hangs the others)."""
+        from . import tlattn as T
+        T.tl_peer_barrier_check(self.flag_ptrs[self.shard.rank])
+
     def __call__(self, q, k, v, causal=False, scale=None, stream=None, pre_barrier=True):
         """Run this rank's shard (local q [B_l, Sq, Hq_l, D], k/v [B_l, Skv, Hkv_l, D]) and
         return the full (O, LSE) views of this rank's buffer, complete on `stream`."""
         import math
 
         from . import tlattn as T
+        if q.dim() != 4 or k.dim() != 4 or v.dim() != 4 or k.shape != v.shape:
+            raise ValueError("expected BSHD q[B_l,Sq,Hq_l,D], k/v[B_l,Skv,Hkv_l,D]")
         Bl, Sq, Hl, D = q.shape
         Skv, Hkvl = k.shape[1], k.shape[2]
+        # the kernel builds every output tensor map from the CALL's sizes: a call that does
+        # not match the buffers allocated here (or this rank's shard) would write past O into
+        # the LSE / flag region of every peer (ADVICE r1), so refuse it before any launch
+        if Sq != self.Sq or D != self.D or q.dtype != self.dtype or k.dtype != self.dtype or \
+                v.dtype != self.dtype:
+            raise ValueError(f"ReplicatedOutput was built for Sq={self.Sq}, D={self.D}, "
+                             f"{self.dtype}; got Sq={Sq}, D={D}, {q.dtype}/{k.dtype}/{v.dtype}")
+        sh = self.shard
+        b_len = len(range(*sh.b.indices(self.B)))
+        hq_len = len(range(*sh.hq.indices(self.Hq)))
+        if Bl != b_len or Hl != hq_len or k.shape[0] != Bl:
+            raise ValueError(f"this rank's shard is B_l={b_len}, Hq_l={hq_len}; got q with "
+                             f"B_l={Bl}, Hq_l={Hl} and k/v with B_l={k.shape[0]}")
+        if Hl % Hkvl != 0:
+            raise ValueError("Hq_l must be a multiple of Hkv_l")
         scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
         B_total, b_off, Hq_total, h_off = replica_layout(self.shard, self.B, self.Hq)
         if pre_barrier:

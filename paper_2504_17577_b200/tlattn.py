@@ -18,7 +18,10 @@ from .build import LIB
 
 TL_DTYPE_F16 = 0
 TL_DTYPE_BF16 = 1
-TL_OK, TL_ERR_INVALID_VALUE, TL_ERR_UNSUPPORTED, TL_ERR_CUDA = 0, 1, 2, 3
+TL_OK, TL_ERR_INVALID_VALUE, TL_ERR_UNSUPPORTED, TL_ERR_CUDA, TL_ERR_TIMEOUT = 0, 1, 2, 3, 4
+TL_PEER_FLAG_WORDS, TL_PEER_STATUS_WORD = 16, 15  # include/tlattn.h
+# experiment / test options (include/tlattn.h tl_option)
+TL_OPT_FORCE_1CTA, TL_OPT_UNIT_TILES, TL_OPT_LPT, TL_OPT_GEMV_TC, TL_OPT_MLA_HC, TL_OPT_MLA_CL = range(6)
 
 _lock = threading.Lock()
 _lib = None
@@ -66,6 +69,14 @@ def load_library(path: str | None = None):
         lib.tl_attn_fwd_replicated.restype = I
         lib.tl_peer_barrier.argtypes = [PP, I, I, ctypes.c_uint32, P]
         lib.tl_peer_barrier.restype = I
+        lib.tl_peer_barrier_set_timeout_ns.argtypes = [U64]
+        lib.tl_peer_barrier_set_timeout_ns.restype = I
+        lib.tl_peer_barrier_check.argtypes = [P]
+        lib.tl_peer_barrier_check.restype = I
+        lib.tl_attn_set_option.argtypes = [I, I]
+        lib.tl_attn_set_option.restype = I
+        lib.tl_attn_get_option.argtypes = [I]
+        lib.tl_attn_get_option.restype = I
         lib.tl_ipc_handle_bytes.argtypes = []
         lib.tl_ipc_handle_bytes.restype = I
         lib.tl_ipc_get_handle.argtypes = [P, P]
@@ -154,9 +165,43 @@ def tl_attn_fwd_replicated(q, k, v, o_outs, lse_outs, B_total, b_off, Hq_total, 
 
 
 def tl_peer_barrier(flags, rank, epoch, stream=None):
-    """Device-side barrier over the ranks whose flag arrays are ``flags`` (one per rank)."""
+    """Device-side barrier over the ranks whose flag arrays are ``flags`` (one per rank,
+    TL_PEER_FLAG_WORDS uint32 each). Bounded: see tl_peer_barrier_check."""
     _check(load_library().tl_peer_barrier(_ptr_array(flags), len(flags), int(rank),
                                           int(epoch) & 0xFFFFFFFF, _stream_handle(stream)))
+
+
+def tl_attn_set_option(option, value):
+    _check(load_library().tl_attn_set_option(int(option), int(value)))
+
+
+def tl_attn_get_option(option) -> int:
+    return int(load_library().tl_attn_get_option(int(option)))
+
+
+class option:
+    """Context manager: set an experiment option (TL_OPT_*) and restore it afterwards."""
+
+    def __init__(self, opt, value):
+        self.opt, self.value = opt, value
+
+    def __enter__(self):
+        self.old = tl_attn_get_option(self.opt)
+        tl_attn_set_option(self.opt, self.value)
+        return self
+
+    def __exit__(self, *a):
+        tl_attn_set_option(self.opt, self.old)
+
+
+def tl_peer_barrier_set_timeout_ns(ns):
+    _check(load_library().tl_peer_barrier_set_timeout_ns(int(ns)))
+
+
+def tl_peer_barrier_check(own_flags):
+    """Synchronise the device and raise TlAttnError(TL_ERR_TIMEOUT) if a barrier on these
+    (own) flags timed out."""
+    _check(load_library().tl_peer_barrier_check(_ptr(own_flags)))
 
 
 def tl_ipc_get_handle(t) -> bytes:
@@ -202,6 +247,23 @@ def _dims(q, k, v):
     return B, Hq, Hkv, Sq, Skv, D
 
 
+def _check_out(t, shape, dtype, device, name):
+    """A caller-provided output must match exactly: the kernels' tensor maps and raw
+    stores are built from the problem sizes, so a smaller or strided buffer would be
+    written out of bounds."""
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != device or \
+            not t.is_contiguous():
+        raise TlAttnError(TL_ERR_INVALID_VALUE,
+                          f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} "
+                          f"on {device} (got {tuple(t.shape)} {t.dtype} on {t.device})")
+
+
+def _same_device(device, *ts):
+    for t in ts:
+        if t is not None and t.device != device:
+            raise TlAttnError(TL_ERR_INVALID_VALUE, f"all tensors must be on {device}")
+
+
 def attention(q, k, v, causal=False, scale=None, return_lse=True, out=None, lse_out=None,
               stream=None):
     """o[, lse] = softmax(scale q k^T [+ causal mask]) v on the GPU (allocates outputs)."""
@@ -209,10 +271,15 @@ def attention(q, k, v, causal=False, scale=None, return_lse=True, out=None, lse_
     if not q.is_cuda:
         raise TlAttnError(TL_ERR_INVALID_VALUE, "attention() takes CUDA tensors; use "
                           "attention_host() for host buffers")
+    _same_device(q.device, k, v)
     scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+    if out is not None:
+        _check_out(out, q.shape, q.dtype, q.device, "out")
     o = out if out is not None else torch.empty_like(q)
     lse = None
     if return_lse:
+        if lse_out is not None:
+            _check_out(lse_out, (B, Hq, Sq), torch.float32, q.device, "lse_out")
         lse = lse_out if lse_out is not None else torch.empty((B, Hq, Sq), dtype=torch.float32,
                                                               device=q.device)
     tl_attn_fwd(q, k, v, o, lse, B, Hq, Hkv, Sq, Skv, D, int(bool(causal)), scale,
@@ -266,15 +333,32 @@ def mla_decode(q, q_pe, kv, k_pe, seqlens=None, scale=None, return_lse=True, out
     for t in (q, q_pe, kv, k_pe):
         if not (t.is_cuda and t.is_contiguous() and t.dtype == q.dtype):
             raise TlAttnError(TL_ERR_INVALID_VALUE, "inputs must be contiguous CUDA tensors of one dtype")
-    if seqlens is not None and (seqlens.dtype != torch.int32 or not seqlens.is_cuda):
-        raise TlAttnError(TL_ERR_INVALID_VALUE, "seqlens must be a CUDA int32 tensor")
+    _same_device(q.device, q_pe, kv, k_pe, seqlens)
+    # every shape the kernel's tensor maps are built from (a shorter k_pe / kv would be read
+    # out of bounds: ADVICE r1)
+    if tuple(q_pe.shape) != (B, H, Dr) or tuple(kv.shape) != (B, Skv, Hkv, Dl) or \
+            tuple(k_pe.shape) != (B, Skv, Hkv, Dr):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "expected q[B,H,Dl], q_pe[B,H,Dr], "
+                          "kv[B,Skv,Hkv,Dl], k_pe[B,Skv,Hkv,Dr] with one B, H, Skv, Hkv")
+    if seqlens is not None and (seqlens.dtype != torch.int32 or not seqlens.is_cuda or
+                                not seqlens.is_contiguous() or seqlens.numel() < B):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "seqlens must be a contiguous CUDA int32 tensor "
+                          "with >= B entries")
     scale = 1.0 / math.sqrt(Dl + Dr) if scale is None else float(scale)
+    if out is not None:
+        _check_out(out, (B, H, Dl), q.dtype, q.device, "out")
     o = out if out is not None else torch.empty((B, H, Dl), dtype=q.dtype, device=q.device)
     lse = None
     if return_lse:
+        if lse_out is not None:
+            _check_out(lse_out, (B, H), torch.float32, q.device, "lse_out")
         lse = lse_out if lse_out is not None else torch.empty((B, H), dtype=torch.float32,
                                                               device=q.device)
     nbytes = tl_mla_decode_workspace_bytes(B, H, Hkv)
+    if workspace is not None and (workspace.dtype != torch.uint8 or
+                                  workspace.device != q.device or not workspace.is_contiguous()):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "workspace must be a contiguous uint8 tensor on "
+                          f"{q.device}")
     if workspace is None:
         workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device)
     tl_mla_decode(q, q_pe, kv, k_pe, o, lse, seqlens, B, H, Hkv, Skv, Dl, Dr, scale,

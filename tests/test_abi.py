@@ -42,8 +42,8 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_version_and_strerror(lib):
-    assert tlattn.tl_attn_version() == 0x000200
-    for code in (0, 1, 2, 3):
+    assert tlattn.tl_attn_version() == 0x000300
+    for code in (0, 1, 2, 3, 4):
         assert tlattn.tl_attn_strerror(code).startswith(("TL_OK", "TL_ERR"))
     assert "unknown" in tlattn.tl_attn_strerror(99)
 
@@ -175,8 +175,27 @@ def test_peer_barrier_and_ipc_invalid_arguments_rejected(lib):
     assert lib.tl_peer_barrier(_ptrs(*([FAKE] * 9)), 9, 0, 1, None) == 1
     assert lib.tl_peer_barrier(_ptrs(FAKE, FAKE), 2, 2, 1, None) == 1
     assert lib.tl_peer_barrier(_ptrs(FAKE, FAKE + 2), 2, 0, 1, None) == 1
+    assert lib.tl_peer_barrier_set_timeout_ns(0) == 1
+    assert lib.tl_peer_barrier_check(None) == 1
+    assert lib.tl_peer_barrier_check(FAKE + 2) == 1
     assert lib.tl_ipc_handle_bytes() >= 64
     buf = ctypes.create_string_buffer(lib.tl_ipc_handle_bytes())
     assert lib.tl_ipc_get_handle(None, buf) == 1
     assert lib.tl_ipc_open_handle(None, None) == 1
     assert lib.tl_ipc_close_handle(None) == 1
+
+
+def test_options_set_get_without_a_device(lib):
+    """Experiment options are process-wide values behind tl_attn_set_option (no getenv on
+    production calls); unknown options are refused, -1 restores automatic."""
+    from paper_2504_17577_b200.tlattn import TL_OPT_LPT, TL_OPT_UNIT_TILES, option
+    assert lib.tl_attn_set_option(99, 1) == 1 and lib.tl_attn_get_option(99) == -2
+    assert lib.tl_attn_set_option(-1, 1) == 1
+    old = lib.tl_attn_get_option(TL_OPT_LPT)
+    with option(TL_OPT_LPT, 1):
+        assert lib.tl_attn_get_option(TL_OPT_LPT) == 1
+        with option(TL_OPT_UNIT_TILES, 2):
+            assert lib.tl_attn_get_option(TL_OPT_UNIT_TILES) == 2
+    assert lib.tl_attn_get_option(TL_OPT_LPT) == old
+    assert lib.tl_attn_set_option(TL_OPT_LPT, -7) == 0 and lib.tl_attn_get_option(TL_OPT_LPT) == -1
+    lib.tl_attn_set_option(TL_OPT_LPT, old)

@@ -77,10 +77,11 @@ def test_mla_scale_values(scale):
 
 
 @pytest.mark.parametrize("hc", ["32", "64"])
-def test_mla_head_tile_widths_agree(hc, monkeypatch):
-    # the same problem through 32-head and 64-head tiles (TLATTN_MLA_HC, read per call)
-    monkeypatch.setenv("TLATTN_MLA_HC", hc)
-    run_and_check(2, 128, 1, 900, BF, gen_seqlens(2, 900, 8), label=f"HC={hc}")
+def test_mla_head_tile_widths_agree(hc):
+    # the same problem through 32-head and 64-head tiles (TL_OPT_MLA_HC)
+    from paper_2504_17577_b200.tlattn import TL_OPT_MLA_HC, option
+    with option(TL_OPT_MLA_HC, int(hc)):
+        run_and_check(2, 128, 1, 900, BF, gen_seqlens(2, 900, 8), label=f"HC={hc}")
 
 
 def test_mla_deterministic_and_zero_length():

@@ -53,13 +53,15 @@ def test_parity_small(B, Hq, Hkv, Sq, Skv, D, dtype, causal):
     (1, 2, 2, 900, 600, False),      # Sq > Skv
 ])
 @pytest.mark.parametrize("tiles", ["1", "2"])
-def test_pair_kernel_unit_modes(B, Hq, Hkv, Sq, Skv, causal, tiles, monkeypatch):
+def test_pair_kernel_unit_modes(B, Hq, Hkv, Sq, Skv, causal, tiles):
     """CTA-pair kernel with 512-row units (2 tiles) and the short-sequence 256-row units
-    (TLATTN_UNIT_TILES forces the mode; read per call): same parity bar on every row."""
-    monkeypatch.setenv("TLATTN_UNIT_TILES", tiles)
+    (TL_OPT_UNIT_TILES forces the mode): same parity bar on every row."""
+    from paper_2504_17577_b200.tlattn import TL_OPT_UNIT_TILES, option, tl_attn_get_option
     q, k, v = gen(B, Hq, Hkv, Sq, Skv, 128, BF, 5 + Sq)
-    check_against_oracle(q, k, v, causal, default_scale(128),
-                         label=f"tiles={tiles} B{B} H{Hq}/{Hkv} S{Sq}x{Skv} c{causal}")
+    with option(TL_OPT_UNIT_TILES, int(tiles)):
+        assert tl_attn_get_option(TL_OPT_UNIT_TILES) == int(tiles)
+        check_against_oracle(q, k, v, causal, default_scale(128),
+                             label=f"tiles={tiles} B{B} H{Hq}/{Hkv} S{Sq}x{Skv} c{causal}")
 
 
 @pytest.mark.parametrize("scale", [0.0, -0.125, 0.37])
@@ -198,14 +200,15 @@ def test_shards_equal_unsharded_slices_bitwise(mode):
 
 
 @pytest.mark.parametrize("causal", [False, True])
-def test_single_cta_kernel_at_d128(causal, monkeypatch):
-    """D=128 normally runs on CTA pairs; the single-CTA kernel (TLATTN_KERNEL=1cta) stays
+def test_single_cta_kernel_at_d128(causal):
+    """D=128 normally runs on CTA pairs; the single-CTA kernel (TL_OPT_FORCE_1CTA) stays
     correct too, and both kernels agree within rounding."""
+    from paper_2504_17577_b200.tlattn import TL_OPT_FORCE_1CTA, option
     q, k, v = gen(2, 4, 2, 700, 700, 128, BF, 91)
     o2, l2 = attention(q, k, v, causal=causal)
-    monkeypatch.setenv("TLATTN_KERNEL", "1cta")
-    check_against_oracle(q, k, v, causal, default_scale(128), label="1cta")
-    o1, l1 = attention(q, k, v, causal=causal)
+    with option(TL_OPT_FORCE_1CTA, 1):
+        check_against_oracle(q, k, v, causal, default_scale(128), label="1cta")
+        o1, l1 = attention(q, k, v, causal=causal)
     torch.cuda.synchronize()
     assert (o1.float() - o2.float()).abs().max().item() < 2e-2
     assert (l1 - l2).abs().max().item() < 1e-4
@@ -260,7 +263,7 @@ def test_concurrent_streams():
 
 
 @pytest.mark.parametrize("D,dtype", [(128, BF), (64, F16)])
-def test_unit_order_does_not_change_results(D, dtype, monkeypatch):
+def test_unit_order_does_not_change_results(D, dtype):
     """The LPT (query-block-major) and the (b, h)-major unit orders schedule the same
     units differently over persistent CTAs that each run several units; every unit's
     arithmetic is the same, so O and LSE must be bitwise equal. Both orders are also
@@ -269,9 +272,10 @@ def test_unit_order_does_not_change_results(D, dtype, monkeypatch):
     B, Hq, Hkv, S = 4, 16, 4, 2048  # 256 pair units / 512 single-CTA units: several per CTA
     q, k, v = gen(B, Hq, Hkv, S, S, D, dtype, 303 + D)
     outs = {}
+    from paper_2504_17577_b200.tlattn import TL_OPT_LPT, option
     for order in ("0", "1"):
-        monkeypatch.setenv("TLATTN_LPT", order)
-        outs[order] = attention(q, k, v, causal=True)
+        with option(TL_OPT_LPT, int(order)):
+            outs[order] = attention(q, k, v, causal=True)
     torch.cuda.synchronize()
     assert torch.equal(outs["0"][0].view(torch.int16), outs["1"][0].view(torch.int16))
     assert torch.equal(outs["0"][1], outs["1"][1])

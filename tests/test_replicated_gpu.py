@@ -151,7 +151,7 @@ def test_replicated_bad_args():
         tl_attn_fwd_replicated(q, q, q, [o] * 9, None, 1, 0, 4, 0, 1, 2, 2, 128, 128, 128, 0, 0.1, 1)
 
 
-def test_replicated_single_cta_after_gemm(monkeypatch):
+def test_replicated_single_cta_after_gemm():
     """Regression: each kernel instantiation sets its dynamic-shared-memory attribute once
     per device; the replicated-output instantiations once shared the GEMM's slots, so a GEMM
     call first left the replicated single-CTA kernel without its attribute."""
@@ -160,12 +160,13 @@ def test_replicated_single_cta_after_gemm(monkeypatch):
     from paper_2504_17577_b200.tlattn import dtype_code
     a = torch.randn(256, 256, device="cuda").to(torch.bfloat16)
     gemm(a, a)
-    monkeypatch.setenv("TLATTN_KERNEL", "1cta")
+    from paper_2504_17577_b200.tlattn import TL_OPT_FORCE_1CTA, option
     B, Hq, Hkv, S, D = 1, 2, 1, 300, 128
     q, k, v = gen_qkv(B, Hq, Hkv, S, S, D, torch.bfloat16, 12, "cuda")
-    o_ref, _ = attention(q, k, v, causal=True)
-    out = torch.zeros_like(o_ref)
-    tl_attn_fwd_replicated(q, k, v, [out], None, B, 0, Hq, 0, B, Hq, Hkv, S, S, D, 1, D ** -0.5,
-                           dtype_code(q.dtype))
+    with option(TL_OPT_FORCE_1CTA, 1):
+        o_ref, _ = attention(q, k, v, causal=True)
+        out = torch.zeros_like(o_ref)
+        tl_attn_fwd_replicated(q, k, v, [out], None, B, 0, Hq, 0, B, Hq, Hkv, S, S, D, 1,
+                               D ** -0.5, dtype_code(q.dtype))
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), o_ref.view(torch.int16))
