@@ -80,6 +80,23 @@ int oracle_mla_brute(const uint16_t* q, const uint16_t* q_pe, const uint16_t* kv
                      long Hkv, long Skv, long Dl, long Dr, double scale, long b, double* s_out,
                      double* p_out, double* o_out, double* lse_out);
 
+/* Mamba-2 SSD chunk kernels (Table 4), see ssd_oracle.c for
+ * the definitions and readings L1-L8. All arrays double; layouts:
+ *   x[B][L][H][P], Bm / C [B][L][G][N], dt / dA [B][H][nchunks][Q], cb [B][nchunks][G][Q][Q],
+ *   states / prev [B][nchunks][H][P][N], D[H] (or NULL), out / y [B][L][H][P].
+ * nchunks = ceil(L / Q); group of head h: h / (H / G). */
+int oracle_ssd_chunk_state(const double* x, const double* Bm, const double* dt, const double* dA,
+                           long B, long L, long H, long G, long P, long N, long Q,
+                           double* states);
+int oracle_ssd_chunk_scan(const double* cb, const double* x, const double* dt, const double* dA,
+                          const double* C, const double* prev, const double* D, long B, long L,
+                          long H, long G, long P, long N, long Q, double* out);
+/* The SSM recurrence position by position (no chunks): dtv[B][L][H], A[H];
+ * y_out [B][L][H][P], h_out [B][H][P][N] (final state) or NULL. */
+int oracle_ssd_recurrence(const double* x, const double* dtv, const double* A, const double* Bm,
+                          const double* C, const double* D, long B, long L, long H, long G,
+                          long P, long N, double* y_out, double* h_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ ORACLE_BF16 = 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "attn_oracle.c"), os.path.join(_HERE, "gemm_oracle.c"),
-        os.path.join(_HERE, "mla_oracle.c")]
+        os.path.join(_HERE, "mla_oracle.c"), os.path.join(_HERE, "ssd_oracle.c")]
 _lock = threading.Lock()
 _lib = None
 
@@ -64,6 +64,14 @@ def _load():
             lib.oracle_mla_brute.argtypes = [P16, P16, P16, P16, I, PI, L, L, L, L, L, L, D, L,
                                              PD, PD, PD, PD]
             lib.oracle_mla_brute.restype = I
+            lib.oracle_ssd_chunk_state.argtypes = [PD, PD, PD, PD, L, L, L, L, L, L, L, PD]
+            lib.oracle_ssd_chunk_state.restype = I
+            lib.oracle_ssd_chunk_scan.argtypes = [PD, PD, PD, PD, PD, PD, PD, L, L, L, L, L, L,
+                                                  L, PD]
+            lib.oracle_ssd_chunk_scan.restype = I
+            lib.oracle_ssd_recurrence.argtypes = [PD, PD, PD, PD, PD, PD, L, L, L, L, L, L, PD,
+                                                  PD]
+            lib.oracle_ssd_recurrence.restype = I
             _lib = lib
     return _lib
 
@@ -245,3 +253,65 @@ def mla_brute(q, q_pe, kv, k_pe, dtype, scale, b, seqlens=None):
     if rc != 0:
         raise ValueError(f"oracle_mla_brute rejected its arguments (rc={rc})")
     return S, P, O, lse
+
+
+# --------------------------------------------------------------------------- Mamba-2 SSD
+# (Table 4; definitions and readings L1-L8 in ssd_oracle.c)
+def _d(a):
+    return np.ascontiguousarray(np.asarray(a, np.float64))
+
+
+def ssd_chunk_state(x, Bm, dt, dA, Q):
+    """states[B][nc][H][P][N] (fp64) of every chunk; x[B,L,H,P], Bm[B,L,G,N],
+    dt/dA[B,H,nc,Q] (any float arrays, widened to fp64)."""
+    x, Bm, dt, dA = _d(x), _d(Bm), _d(dt), _d(dA)
+    Bn, L, H, P = x.shape
+    G, N = Bm.shape[2], Bm.shape[3]
+    nc = (L + Q - 1) // Q
+    assert Bm.shape[:2] == (Bn, L) and dt.shape == (Bn, H, nc, Q) and dA.shape == dt.shape
+    out = np.zeros((Bn, nc, H, P, N), np.float64)
+    rc = _load().oracle_ssd_chunk_state(_pd(x), _pd(Bm), _pd(dt), _pd(dA), Bn, L, H, G, P, N,
+                                        Q, _pd(out))
+    if rc != 0:
+        raise ValueError("oracle_ssd_chunk_state rejected its arguments")
+    return out
+
+
+def ssd_chunk_scan(cb, x, dt, dA, C, prev, D, Q):
+    """out[B][L][H][P] (fp64); cb[B,nc,G,Q,Q], prev[B,nc,H,P,N], D[H] or None."""
+    cb, x, dt, dA, C, prev = _d(cb), _d(x), _d(dt), _d(dA), _d(C), _d(prev)
+    Dd = None if D is None else _d(D)
+    Bn, L, H, P = x.shape
+    G, N = C.shape[2], C.shape[3]
+    nc = (L + Q - 1) // Q
+    assert cb.shape == (Bn, nc, G, Q, Q) and prev.shape == (Bn, nc, H, P, N)
+    assert C.shape[:2] == (Bn, L) and dt.shape == (Bn, H, nc, Q) and dA.shape == dt.shape
+    out = np.zeros((Bn, L, H, P), np.float64)
+    rc = _load().oracle_ssd_chunk_scan(_pd(cb), _pd(x), _pd(dt), _pd(dA), _pd(C), _pd(prev),
+                                       _pd(Dd), Bn, L, H, G, P, N, Q, _pd(out))
+    if rc != 0:
+        raise ValueError("oracle_ssd_chunk_scan rejected its arguments")
+    return out
+
+
+def ssd_recurrence(x, dtv, A, Bm, C, D):
+    """The SSM recurrence position by position: (y[B,L,H,P], final state h[B,H,P,N])."""
+    x, dtv, A, Bm, C = _d(x), _d(dtv), _d(A), _d(Bm), _d(C)
+    Dd = None if D is None else _d(D)
+    Bn, L, H, P = x.shape
+    G, N = Bm.shape[2], Bm.shape[3]
+    y = np.zeros((Bn, L, H, P), np.float64)
+    hf = np.zeros((Bn, H, P, N), np.float64)
+    rc = _load().oracle_ssd_recurrence(_pd(x), _pd(dtv), _pd(A), _pd(Bm), _pd(C), _pd(Dd), Bn, L,
+                                       H, G, P, N, _pd(y), _pd(hf))
+    if rc != 0:
+        raise ValueError("oracle_ssd_recurrence rejected its arguments")
+    return y, hf
+
+
+def ssd_sample_chunks(fn, pairs, threads=None):
+    """Run fn(b, c) for the given (b, c) pairs on host threads; returns {(b, c): result}."""
+    threads = threads or len(os.sched_getaffinity(0))
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(lambda bc: (bc, fn(*bc)), pairs))
+    return dict(res)

@@ -20,7 +20,10 @@ import math
 import numpy as np
 import torch
 
-TENSOR_ID = {"q": 1, "k": 2, "v": 3, "q_pe": 4, "kv": 5, "k_pe": 6, "seqlens": 7}
+TENSOR_ID = {"q": 1, "k": 2, "v": 3, "q_pe": 4, "kv": 5, "k_pe": 6, "seqlens": 7,
+             # Mamba-2 SSD chunk kernels (reading L8)
+             "ssd_x": 8, "ssd_B": 9, "ssd_C": 10, "ssd_dt": 11, "ssd_A": 12, "ssd_D": 13,
+             "ssd_cb": 14, "ssd_prev": 15}
 _M32 = 0xFFFFFFFF
 
 
@@ -52,6 +55,13 @@ def normal_from_index(idx: torch.Tensor, seed: int, tensor_id: int) -> torch.Ten
     u2 = ((h1 >> 8).to(torch.float32) + 0.5) * (1.0 / 16777216.0)
     r = torch.sqrt(-2.0 * torch.log(u1))
     return r * torch.cos((2.0 * math.pi) * u2)
+
+
+def uniform_from_index(idx: torch.Tensor, seed: int, tensor_id: int) -> torch.Tensor:
+    """U(0, 1) fp32 values (open interval) for int64 global indices (any device)."""
+    key = _key(seed, tensor_id)
+    h = _lowbias32(_lowbias32((idx & _M32) ^ key) ^ ((idx >> 31) & _M32))
+    return ((h >> 8).to(torch.float32) + 0.5) * (1.0 / 16777216.0)
 
 
 def gen_tensor(shape, seed: int, name: str, dtype: torch.dtype, device,
@@ -133,3 +143,48 @@ def to_bits(t: torch.Tensor) -> np.ndarray:
 def from_values(values, dtype: torch.dtype, device="cpu") -> torch.Tensor:
     """Tensor of the given (float) values rounded RN to ``dtype``."""
     return torch.as_tensor(np.asarray(values, dtype=np.float32)).to(dtype).to(device)
+
+
+def gen_ssd(B, L, H, G, P, N, dtype, seed, device):
+    """Mamba-2 SSD inputs (Table 4; reading L8), drawn like the
+    Mamba-2 initialisation: x[B,L,H,P], Bm / C [B,L,G,N] iid N(0,1) rounded to ``dtype``;
+    per-position step sizes dt[B,L,H] log-uniform in [1e-3, 1e-1] (fp32); A[H] = -U[1, 16]
+    (fp32); D[H] = U[0.5, 1.5] (fp32)."""
+    x = gen_tensor((B, L, H, P), seed, "ssd_x", dtype, device)
+    Bm = gen_tensor((B, L, G, N), seed, "ssd_B", dtype, device)
+    C = gen_tensor((B, L, G, N), seed, "ssd_C", dtype, device)
+    n_dt = B * L * H
+    u = uniform_from_index(torch.arange(n_dt, dtype=torch.int64, device=device), seed,
+                           TENSOR_ID["ssd_dt"])
+    dtv = torch.exp(math.log(1e-3) + u * (math.log(1e-1) - math.log(1e-3))).view(B, L, H)
+    ua = uniform_from_index(torch.arange(H, dtype=torch.int64, device=device), seed,
+                            TENSOR_ID["ssd_A"])
+    A = -(1.0 + 15.0 * ua)
+    ud = uniform_from_index(torch.arange(H, dtype=torch.int64, device=device), seed,
+                            TENSOR_ID["ssd_D"])
+    D = 0.5 + ud
+    return x, Bm, C, dtv.float(), A.float(), D.float()
+
+
+def ssd_chunked_dt(dtv, A, Q):
+    """The chunked step-size and cumulative-decay inputs of both chunk kernels (reading L4):
+    dt[B,H,nc,Q] and dA[b,h,c,i] = sum_{j <= i} dt A_h inside chunk c (fp32; entries past the
+    sequence end are 0). Input preparation (Mamba-2 computes dA_cumsum before the chunk
+    kernels); accumulated in fp64 on the tensor's device, then rounded to fp32."""
+    Bn, L, H = dtv.shape
+    nc = (L + Q - 1) // Q
+    dt_c = torch.zeros((Bn, nc * Q, H), dtype=torch.float64, device=dtv.device)
+    dt_c[:, :L] = dtv.double()
+    dt_c = dt_c.view(Bn, nc, Q, H).permute(0, 3, 1, 2).contiguous()  # [B, H, nc, Q]
+    dA = torch.cumsum(dt_c * A.double().view(1, H, 1, 1), dim=3)
+    return dt_c.float().contiguous(), dA.float().contiguous()
+
+
+def gen_ssd_cb_prev(B, L, H, G, P, N, dtype, seed, device, Q=256):
+    """Bench-only stand-ins for the two inputs chunk_scan takes from earlier pipeline steps
+    (reading L8): cb[B,nc,G,Q,Q] iid N(0, N) (the spread of a C.B^T entry) and the entering
+    states prev[B,nc,H,P,N] iid N(0,1), both rounded to ``dtype``."""
+    nc = (L + Q - 1) // Q
+    cb = gen_tensor((B, nc, G, Q, Q), seed, "ssd_cb", torch.float32, device) * math.sqrt(N)
+    prev = gen_tensor((B, nc, H, P, N), seed, "ssd_prev", dtype, device)
+    return cb.to(dtype), prev
