@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define TLATTN_VERSION 0x000300 /* 0.3.0: bounded tl_peer_barrier (+ _set_timeout_ns, _check); tl_attn_set/get_option */
+#define TLATTN_VERSION 0x000300 /* 0.3.0: bounded tl_peer_barrier (+ _set_timeout_ns, _check); tl_attn_set/get_option; tl_ssd_chunk_state / _scan */
 
 enum tl_dtype { TL_DTYPE_F16 = 0, TL_DTYPE_BF16 = 1 };
 
@@ -242,6 +242,49 @@ int tl_ipc_handle_bytes(void);
 int tl_ipc_get_handle(const void* dev_ptr, void* handle_out);
 int tl_ipc_open_handle(const void* handle, void** dev_ptr_out);
 int tl_ipc_close_handle(void* dev_ptr);
+
+/*
+ * Mamba-2 SSD chunk kernels ("linear attention"): the chunk-state and
+ * chunk-scan functions of Mamba-2 the paper benchmarks (§5.2, Table 4
+ * P:L464-478). The paper prints no formula; the definitions below are the Mamba-2 SSD
+ * chunked algorithm for the scalar-decay SSM h_t = exp(dt_t A_h) h_{t-1} + dt_t B_t x_t^T,
+ * y_t = C_t^T h_t + D_h x_t (readings L1-L8). Chunk c covers positions
+ * [cQ, cQ + len_c), len_c = min(Q, seqlen - cQ); nchunks = ceil(seqlen / Q); head h uses
+ * group g = h / (nheads / ngroups).
+ *
+ * tl_ssd_chunk_state:
+ *   states[b,c,h,p,n] = sum_{i < len_c} x[b,cQ+i,h,p] Bm[b,cQ+i,g,n]
+ *                        * exp(dA[b,h,c,len_c-1] - dA[b,h,c,i]) * dt[b,h,c,i]
+ * tl_ssd_chunk_scan:
+ *   out[b,cQ+i,h,p] = exp(dA[b,h,c,i]) sum_n C[b,cQ+i,g,n] prev[b,c,h,p,n]
+ *                    + sum_{j <= i} cb[b,c,g,i,j] exp(dA[b,h,c,i] - dA[b,h,c,j]) dt[b,h,c,j] x[b,cQ+j,h,p]
+ *                    + D[h] x[b,cQ+i,h,p]
+ *
+ *   x       [batch][seqlen][nheads][headdim]            16-bit (dtype), 16-byte aligned
+ *   Bm, C   [batch][seqlen][ngroups][dstate]            16-bit
+ *   dt, dA  [batch][nheads][nchunks][chunk_size] fp32 (dt > 0: the step sizes; dA: the
+ *           inclusive cumulative sum of dt * A_h inside each chunk); entries i >= len_c of
+ *           the last chunk are ignored
+ *   cb      [batch][nchunks][ngroups][chunk_size][chunk_size] 16-bit (C B^T per chunk)
+ *   prev_states / states [batch][nchunks][nheads][headdim][dstate] 16-bit
+ *   D       [nheads] fp32, or NULL (no skip term)
+ *   out     [batch][seqlen][nheads][headdim] 16-bit
+ * fp32 accumulation; chunk_state rounds each state RN to dtype, chunk_scan each output.
+ * Supported: headdim = 64, dstate = 128, chunk_size = 256 (Table 4 / reading L2), fp16 or
+ * bf16, nheads % ngroups == 0; chunk_state also needs nheads / ngroups even (the two
+ * heads of a CTA's head pair share one group's Bm tile).
+ * One kernel launch each, stream-ordered, no allocation, graph-capturable; the caller owns
+ * every buffer. Errors: TL_ERR_INVALID_VALUE (NULL pointers, sizes < 1, nheads % ngroups,
+ * bad dtype), TL_ERR_UNSUPPORTED (headdim / dstate / chunk_size / odd nheads / ngroups, misaligned
+ * pointers, sizes beyond 32-bit TMA coordinates, device not sm_100), TL_ERR_CUDA.
+ */
+int tl_ssd_chunk_state(const void* x, const void* Bm, const float* dt, const float* dA,
+                       void* states, int batch, int seqlen, int nheads, int ngroups, int headdim,
+                       int dstate, int chunk_size, int dtype, void* stream);
+int tl_ssd_chunk_scan(const void* cb, const void* x, const float* dt, const float* dA,
+                      const void* C, const void* prev_states, const float* D, void* out,
+                      int batch, int seqlen, int nheads, int ngroups, int headdim, int dstate,
+                      int chunk_size, int dtype, void* stream);
 
 /* Static, NUL-terminated description of a tl_status code. Never NULL. */
 const char* tl_attn_strerror(int status);

@@ -20,6 +20,10 @@ from .tlattn import (  # noqa: F401
     tl_mla_decode,
     tl_mla_decode_workspace_bytes,
     tl_gemm,
+    ssd_chunk_state,
+    ssd_chunk_scan,
+    tl_ssd_chunk_state,
+    tl_ssd_chunk_scan,
     load_library,
     tl_attn_fwd,
     tl_attn_fwd_host,

@@ -1,0 +1,596 @@
+// ssd_sm100.cuh — Mamba-2 SSD chunk kernels ("linear attention"):
+// chunk_state and chunk_scan (§5.2: "the chunk-scan and chunk-state
+// functions from Mamba-2"; shapes Table 4). Definitions: include/tlattn.h,
+// readings L1-L8 in DESIGN.md §3.
+//
+//   chunk_state:  states[b,c,h,p,n] = sum_{i < len_c} x[b,cQ+i,h,p] B[b,cQ+i,g,n] w[i],
+//                 w[i] = exp(dA[b,h,c,len_c-1] - dA[b,h,c,i]) dt[b,h,c,i]
+//   chunk_scan:   out[b,cQ+i,h,p] = exp(dA[i]) sum_n C[b,cQ+i,g,n] prev[b,c,h,p,n]
+//                   + sum_{j <= i} cb[b,c,g,i,j] exp(dA[i] - dA[j]) dt[j] x[b,cQ+j,h,p]
+//                   + D[h] x[b,cQ+i,h,p]
+//
+// Both are batched GEMMs whose operands need a per-row (state) or per-element (scan) decay
+// factor first, and both are HBM-bound at the Table 4 shapes (~80-100 FLOP/B): the design
+// goal is to stream x / states / out at HBM speed with the contraction on tcgen05.
+//
+// B200 design (single-CTA tcgen05, M = 128; persistent CTAs striding over units):
+//   * chunk_state unit = (b, c, head pair): A = x'^T [M = 2 heads x 64 p][K = Q positions]
+//     with x' = w[i] x (each x row scaled in SMEM by "scale" warps: the TMA box [64 t][64 p]
+//     is exactly the MN-major SWIZZLE_128B A operand, a row stays a row under the swizzle),
+//     B = Bm [N = 128 n][K] (MN-major), D = states in TMEM (double-buffered over units), the
+//     epilogue warps convert and store each (h, p) row (256 B). Consecutive units share (b, c),
+//     so the Bm tile of a chunk is read from HBM once and from L2 by the other head pairs.
+//   * chunk_scan unit = (b, c, h), two M = 128 row tiles: O1 = C [m][n] . prev [p][n]^T
+//     (both K-major, K = n = 128), O2 = W [m][k] . x [k][p] (x MN-major, K = k) with
+//     W = cb . exp(dA[m] - dA[k]) dt[k] . [k <= m] built in SMEM over the cb tile by eight
+//     "W" warps (one row per thread, two threads per row: 64 k each); the causal structure
+//     skips the (m0, k1) block. The epilogue warps form out = exp(dA[m]) O1 + O2 + D x.
+//   * every operand streams through one ring of 16 KB TMA slots (per-slot full / empty
+//     barriers; the six W half-blocks of a unit also have "built" barriers) in one fixed
+//     per-unit order that the producer, W warps and MMA warp all follow.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace tlattn {
+namespace ssd {
+
+constexpr int P = 64;     // head_dim (Table 4)
+constexpr int N = 128;    // d_state (Table 4)
+constexpr int Q = 256;    // chunk length (reading L2)
+constexpr uint32_t SLOT = 16384;
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct SsdParams {
+  CUtensorMap tm_x;   // x  [B][L][H][P]  as (P, H, L, B)
+  CUtensorMap tm_b;   // Bm [B][L][G][N]  as (N, G, L, B)       (chunk_state)
+  CUtensorMap tm_c;   // C  [B][L][G][N]  as (N, G, L, B)       (chunk_scan)
+  CUtensorMap tm_cb;  // cb [B][nc][G][Q][Q] as (Q k, Q m, G, B*nc)  (chunk_scan)
+  CUtensorMap tm_s;   // prev [B][nc][H][P][N] as (N, P, H, B*nc)   (chunk_scan)
+  const float* dt;    // [B][H][nc][Q]
+  const float* dA;    // [B][H][nc][Q]
+  const float* D;     // [H] or nullptr (chunk_scan)
+  const void* x;      // raw x (chunk_scan epilogue: D x)
+  void* out;          // states [B][nc][H][P][N] (state) / out [B][L][H][P] (scan)
+  int B, L, H, G, nc, grp;  // grp = H / G
+  int n_units;
+};
+
+template <bool BF16>
+__device__ __forceinline__ float2 unpack2(uint32_t v) {
+  if constexpr (BF16) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
+    return __bfloat1622float2(h);
+  } else {
+    __half2 h = *reinterpret_cast<__half2*>(&v);
+    return __half22float2(h);
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack2rn(float lo, float hi) {
+  uint32_t r;
+  if constexpr (BF16) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  else asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+// ============================================================================ chunk_state
+struct StateCfg {
+  static constexpr int NSLOT = 12;                  // 16 KB slots (a stage = 2 slots)
+  static constexpr int STAGES = Q / 64;             // 64 positions per stage
+  static constexpr int OFF_RING = 0;
+  static constexpr int OFF_BAR = OFF_RING + NSLOT * SLOT;
+  // full[NSLOT/2] scaled[NSLOT/2] empty[NSLOT/2] acc_full[2] acc_empty[2]
+  static constexpr int NST = NSLOT / 2;             // stages in flight
+  static constexpr int NUM_BARS = 3 * NST + 4;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
+  static constexpr int THREADS = 384;  // 0 TMA, 1 MMA, 4-7 scale, 8-11 epilogue
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+};
+
+template <bool BF16>
+__global__ void __launch_bounds__(StateCfg::THREADS, 1)
+tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
+  using C = StateCfg;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  if ((base & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1024-B alignment
+  const uint32_t sRing = base + C::OFF_RING;
+  const uint32_t bar0 = base + C::OFF_BAR;
+  auto bar_full = [&](int s) { return bar0 + 8u * s; };
+  auto bar_scaled = [&](int s) { return bar0 + 8u * (C::NST + s); };
+  auto bar_empty = [&](int s) { return bar0 + 8u * (2 * C::NST + s); };
+  auto bar_acc_full = [&](int i) { return bar0 + 8u * (3 * C::NST + i); };
+  auto bar_acc_empty = [&](int i) { return bar0 + 8u * (3 * C::NST + 2 + i); };
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int H2 = p.H >> 1;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_x);
+    prefetch_tmap(&p.tm_b);
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_scaled(s), 4);
+      mbar_init(bar_empty(s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_acc_full(i), 1);
+      mbar_init(bar_acc_empty(i), 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<256>(smem_u32(tmem_ptr_smem));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_smem;
+
+  // unit u -> (b, c, head pair hp); consecutive units share (b, c): Bm of the chunk from L2
+  auto decode = [&](int u, int& b, int& c, int& hp) {
+    hp = u % H2;
+    const int bc = u / H2;
+    c = bc % p.nc;
+    b = bc / p.nc;
+  };
+
+  if (warp == 0) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      int it = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        int b, c, hp;
+        decode(u, b, c, hp);
+        const int h0 = 2 * hp, g = h0 / p.grp;
+        for (int st = 0; st < C::STAGES; ++st, ++it) {
+          const int s = it % C::NST;
+          if (it >= C::NST) mbar_wait(bar_empty(s), ((it / C::NST) - 1) & 1);
+          mbar_arrive_expect_tx(bar_full(s), 2 * SLOT);
+          const uint32_t dst = sRing + s * 2 * SLOT;
+          const int t0 = c * Q + st * 64;
+          // x rows [t0, t0+64) of heads h0, h0+1 (OOB rows past L zero-filled), then Bm
+          tma_load_4d(dst, &p.tm_x, bar_full(s), 0, h0, t0, b, pol_x);
+          tma_load_4d(dst + 8192, &p.tm_x, bar_full(s), 0, h0 + 1, t0, b, pol_x);
+          tma_load_4d(dst + SLOT, &p.tm_b, bar_full(s), 0, g, t0, b, pol_b);
+          tma_load_4d(dst + SLOT + 8192, &p.tm_b, bar_full(s), 64, g, t0, b, pol_b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ========== MMA issuer (whole warp; one elected lane issues) ==========
+    constexpr uint32_t FMT = BF16 ? 1u : 0u;
+    // D[m = (head, p)][n] = sum_t x'[t][m] Bm[t][n]: A = x' MN-major, B = Bm MN-major
+    constexpr uint32_t IDESC = make_idesc_f16(FMT, 128, N, 1, 1, 0);
+    int it = 0, lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      const int a = lu & 1;
+      if (lu >= 2) mbar_wait(bar_acc_empty(a), ((lu >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t tm_d = tmem_base + a * N;
+      for (int st = 0; st < C::STAGES; ++st, ++it) {
+        const int s = it % C::NST;
+        mbar_wait(bar_scaled(s), (it / C::NST) & 1);
+        tc_fence_after();
+        const uint32_t xa = sRing + s * 2 * SLOT;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // 16 positions per K step: +16 rows of 128 B
+          if (elect_one())
+            mma_f16_ss(tm_d, make_sdesc_sw128(xa + kk * 2048, 8192, 1024),
+                       make_sdesc_sw128(xa + SLOT + kk * 2048, 8192, 1024), IDESC,
+                       (st > 0 || kk > 0) ? 1u : 0u);
+        if (elect_one()) mma_commit(bar_empty(s));
+      }
+      if (elect_one()) mma_commit(bar_acc_full(a));
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {
+    // ===== scale warps: x row (t, head) *= w[t] = exp(dA[last] - dA[t]) dt[t], in SMEM =====
+    const int i = threadIdx.x - 128;
+    const int r = i & 63, hh = i >> 6;
+    int it = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      int b, c, hp;
+      decode(u, b, c, hp);
+      const int h = 2 * hp + hh;
+      const int len = min(Q, p.L - c * Q);
+      const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
+      const float dA_last = p.dA[vo + len - 1];
+      for (int st = 0; st < C::STAGES; ++st, ++it) {
+        const int s = it % C::NST;
+        const int pos = st * 64 + r;
+        const float w = pos < len ? exp2f((dA_last - p.dA[vo + pos]) * LOG2E) * p.dt[vo + pos] : 0.f;
+        mbar_wait(bar_full(s), (it / C::NST) & 1);
+        // row r of box hh: 128 B (a SW128 row stays one row; only its 16-B units permute)
+        const uint32_t row = sRing + s * 2 * SLOT + hh * 8192 + r * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t v[4];
+          ld_shared_v4(row + q * 16, v);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = unpack2<BF16>(v[e]);
+            v[e] = pack2rn<BF16>(f.x * w, f.y * w);
+          }
+          st_shared_v4(row + q * 16, v[0], v[1], v[2], v[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_scaled(s));
+      }
+    }
+  } else if (warp >= 8) {
+    // ===== epilogue: TMEM lane m = (head h0 + m/64, p = m%64) -> 128 states, RN, global =====
+    const int q4 = warp & 3;
+    const int m = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    int lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      int b, c, hp;
+      decode(u, b, c, hp);
+      const int a = lu & 1;
+      const int h = 2 * hp + (m >> 6), pp = m & 63;
+      mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
+      tc_fence_after();
+      uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) +
+                     ((((size_t)b * p.nc + c) * p.H + h) * P + pp) * (size_t)N * 2;
+#pragma unroll
+      for (int cc = 0; cc < N / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + lane_off + a * N + cc * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack2rn<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_global_v4(dst + cc * 64 + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_acc_empty(a));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem_base);
+  }
+}
+
+// ============================================================================ chunk_scan
+// Per-unit ring items (16 KB slots), in the order the MMA consumes them:
+//   0 S (prev [64 p][128 n], 2 boxes) | 1-2 C rows 0-127 (n halves) | 3 x rows 0-127 |
+//   4-5 cb (m 0-127, k 0-127: k halves) | 6-7 C rows 128-255 | 8-9 cb (m 128-255, k 0-127) |
+//   10 x rows 128-255 | 11-12 cb (m 128-255, k 128-255)
+struct ScanCfg {
+  static constexpr int NSLOT = 12;
+  static constexpr int ITEMS = 13;
+  static constexpr int OFF_RING = 0;
+  static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // dA, log2 dt of the unit: 2 x Q f32
+  static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * Q * 4;   // double-buffered over units
+  // full[NSLOT] empty[NSLOT] built[6] acc_full[2] acc_empty[2] vec_full[2] vec_empty[2].
+  // built[2 * block + k half] completes once per unit (W blocks (m0,k0) (m1,k0) (m1,k1)):
+  // a per-slot "built" barrier would complete only on the slot's W fills and fall out of
+  // step with the fill count that the waiters' parity follows.
+  static constexpr int NUM_BARS = 2 * NSLOT + 6 + 8;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
+  static constexpr int THREADS = 512;  // 0 TMA, 1 MMA, 2 vectors, 4-11 W builders, 12-15 epilogue
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+};
+
+template <bool BF16>
+__global__ void __launch_bounds__(ScanCfg::THREADS, 1)
+tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
+  using C = ScanCfg;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t base = smem_u32(smem_raw);
+  if ((base & 1023u) != 0u) __trap();
+  const uint32_t sRing = base + C::OFF_RING;
+  float* vec = reinterpret_cast<float*>(smem_raw + C::OFF_VEC);  // [buf][dA | log2 dt][Q]
+  const uint32_t bar0 = base + C::OFF_BAR;
+  auto bar_full = [&](int s) { return bar0 + 8u * s; };
+  auto bar_empty = [&](int s) { return bar0 + 8u * (C::NSLOT + s); };
+  auto bar_built = [&](int w) { return bar0 + 8u * (2 * C::NSLOT + w); };
+  auto bar_acc_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 6 + i); };
+  auto bar_acc_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + i); };
+  auto bar_vec_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 10 + i); };
+  auto bar_vec_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 12 + i); };
+  uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tm_x);
+    prefetch_tmap(&p.tm_c);
+    prefetch_tmap(&p.tm_cb);
+    prefetch_tmap(&p.tm_s);
+    for (int s = 0; s < C::NSLOT; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_empty(s), 1);
+    }
+    for (int w = 0; w < 6; ++w) mbar_init(bar_built(w), 4);  // the 4 W warps of one k half
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_acc_full(i), 1);
+      mbar_init(bar_acc_empty(i), 4);
+      mbar_init(bar_vec_full(i), 1);
+      mbar_init(bar_vec_empty(i), 8 + 4);  // W warps + epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(smem_u32(tmem_ptr_smem));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_smem;
+
+  // unit u -> (b, c, h); consecutive units share (b, c): C and cb of the chunk from L2
+  auto decode = [&](int u, int& b, int& c, int& h) {
+    h = u % p.H;
+    const int bc = u / p.H;
+    c = bc % p.nc;
+    b = bc / p.nc;
+  };
+
+  if (warp == 0) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      const uint64_t pol_s = policy_evict_first();   // x, prev: read once
+      const uint64_t pol_l = policy_evict_last();    // C, cb: re-read by the chunk's other heads
+      int f = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        int b, c, h;
+        decode(u, b, c, h);
+        const int g = h / p.grp;
+        const int bc = b * p.nc + c;
+        for (int item = 0; item < C::ITEMS; ++item, ++f) {
+          const int s = f % C::NSLOT;
+          if (f >= C::NSLOT) mbar_wait(bar_empty(s), ((f / C::NSLOT) - 1) & 1);
+          mbar_arrive_expect_tx(bar_full(s), SLOT);
+          const uint32_t dst = sRing + s * SLOT;
+          const uint32_t fb = bar_full(s);
+          switch (item) {
+            case 0:  // prev [64 p][128 n]: two [64 p][64 n] boxes
+              tma_load_4d(dst, &p.tm_s, fb, 0, 0, h, bc, pol_s);
+              tma_load_4d(dst + 8192, &p.tm_s, fb, 64, 0, h, bc, pol_s);
+              break;
+            case 1: case 2: case 6: case 7: {  // C [128 t][64 n] (n half, row tile)
+              const int mt = item >= 6, nh = (item - (mt ? 6 : 1));
+              tma_load_4d(dst, &p.tm_c, fb, 64 * nh, g, c * Q + 128 * mt, b, pol_l);
+              break;
+            }
+            case 3: case 10: {  // x [128 k][64 p]
+              const int kt = item == 10;
+              tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * kt, b, pol_s);
+              break;
+            }
+            default: {  // cb [128 m][64 k]: items 4,5 (m0 k0), 8,9 (m1 k0), 11,12 (m1 k1)
+              const int mt = item >= 8, kt = item >= 11;
+              const int kh = (item == 5 || item == 9 || item == 12);
+              tma_load_4d(dst, &p.tm_cb, fb, 128 * kt + 64 * kh, 128 * mt, g, bc, pol_l);
+              break;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ========== MMA issuer (whole warp; one elected lane issues) ==========
+    constexpr uint32_t FMT = BF16 ? 1u : 0u;
+    constexpr uint32_t IDESC1 = make_idesc_f16(FMT, 128, P, 0, 0, 0);  // C . prev^T (K-major)
+    constexpr uint32_t IDESC2 = make_idesc_f16(FMT, 128, P, 0, 1, 0);  // W . x (x MN-major)
+    int f = 0, lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu, f += C::ITEMS) {
+      const int a = lu & 1;
+      if (lu >= 2) mbar_wait(bar_acc_empty(a), ((lu >> 1) - 1) & 1);
+      tc_fence_after();
+      auto slot = [&](int item) { return (f + item) % C::NSLOT; };
+      auto par = [&](int item) { return ((f + item) / C::NSLOT) & 1; };
+      auto saddr = [&](int item) { return sRing + slot(item) * SLOT; };
+      const uint32_t acc = tmem_base + a * 256;  // [O1 m0 | O2 m0 | O1 m1 | O2 m1] x 64 cols
+      // O1[mt] = C[mt rows] . prev^T: A items (ca, cb_) = n halves, B = item 0
+      auto gemm1 = [&](int mt, int ia, int ib) {
+        mbar_wait(bar_full(slot(0)), par(0));
+        mbar_wait(bar_full(slot(ia)), par(ia));
+        mbar_wait(bar_full(slot(ib)), par(ib));
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < N / 16; ++kk) {
+          const uint32_t asrc = saddr(kk < 4 ? ia : ib) + (kk & 3) * 32;
+          const uint32_t bsrc = saddr(0) + (kk >> 2) * 8192 + (kk & 3) * 32;
+          if (elect_one())
+            mma_f16_ss(acc + 128 * mt, make_sdesc_sw128(asrc, 16, 1024),
+                       make_sdesc_sw128(bsrc, 16, 1024), IDESC1, kk > 0 ? 1u : 0u);
+        }
+      };
+      // O2[mt] += W[mt][kt] . x[kt]: A items (wa, wb) = k halves of W block wblk (built),
+      // B = x item
+      auto gemm2 = [&](int mt, int wblk, int wa, int wb, int xi, bool first) {
+        mbar_wait(bar_full(slot(xi)), par(xi));
+        mbar_wait(bar_built(2 * wblk), lu & 1);
+        mbar_wait(bar_built(2 * wblk + 1), lu & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t asrc = saddr(kk < 4 ? wa : wb) + (kk & 3) * 32;
+          const uint32_t bsrc = saddr(xi) + kk * 2048;
+          if (elect_one())
+            mma_f16_ss(acc + 128 * mt + 64, make_sdesc_sw128(asrc, 16, 1024),
+                       make_sdesc_sw128(bsrc, 16, 1024), IDESC2, (!first || kk > 0) ? 1u : 0u);
+        }
+      };
+      auto release = [&](int item) {
+        if (elect_one()) mma_commit(bar_empty(slot(item)));
+      };
+      gemm1(0, 1, 2);
+      release(1), release(2);
+      gemm2(0, 0, 4, 5, 3, true);
+      release(4), release(5);
+      gemm1(1, 6, 7);
+      release(0), release(6), release(7);
+      gemm2(1, 1, 8, 9, 3, true);
+      release(3), release(8), release(9);
+      gemm2(1, 2, 11, 12, 10, false);
+      release(10), release(11), release(12);
+      if (elect_one()) mma_commit(bar_acc_full(a));
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ====== unit vectors: dA and log2(dt) of (b, h, c) into SMEM (double-buffered) ======
+    int lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      int b, c, h;
+      decode(u, b, c, h);
+      const int vb = lu & 1;
+      if (lu >= 2) mbar_wait(bar_vec_empty(vb), ((lu >> 1) - 1) & 1);
+      const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
+      float* dst = vec + vb * 2 * Q;
+      for (int i = lane; i < Q; i += 32) {
+        dst[i] = p.dA[vo + i];
+        dst[Q + i] = __log2f(p.dt[vo + i]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_vec_full(vb));  // release: smem writes visible to waiters
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ===== W builders: row m of a cb block, k half kh: W = cb exp2((dA[m]-dA[k]) log2e + log2 dt[k]) [k <= m, k < len]
+    const int q4 = warp & 3;
+    const int kh = (warp - 4) >> 2;  // k half of each cb block this warp builds
+    const int r = q4 * 32 + lane;    // row within the 128-row tile
+    int f = 0, lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu, f += C::ITEMS) {
+      int b, c, h;
+      decode(u, b, c, h);
+      const int len = min(Q, p.L - c * Q);
+      const int vb = lu & 1;
+      mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
+      const float* vdA = vec + vb * 2 * Q;
+      const float* vlt = vdA + Q;
+      // blocks (mt, kt, item of this warp's k half)
+      const int blk_mt[3] = {0, 1, 1}, blk_kt[3] = {0, 0, 1};
+      const int blk_it[3] = {4 + kh, 8 + kh, 11 + kh};
+#pragma unroll
+      for (int bi = 0; bi < 3; ++bi) {
+        const int item = blk_it[bi];
+        const int s = (f + item) % C::NSLOT;
+        mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
+        const int m = blk_mt[bi] * 128 + r;             // row within the chunk
+        const int k0 = blk_kt[bi] * 128 + 64 * kh;     // first key (column) of this half
+        const float am = vdA[min(m, Q - 1)] * LOG2E;
+        const uint32_t row = sRing + s * SLOT + r * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // 16-B unit q of the row holds keys 8 (q ^ (r & 7)) ..
+          const int kb = k0 + 8 * (q ^ (r & 7));
+          uint32_t v[4];
+          if (kb > m || kb >= len) {  // the whole unit is masked (above the diagonal / past len)
+            v[0] = v[1] = v[2] = v[3] = 0u;
+          } else {
+            ld_shared_v4(row + q * 16, v);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = kb + 2 * e;
+              const float2 cbv = unpack2<BF16>(v[e]);
+              const float w0 = (k <= m && k < len) ? cbv.x * exp2f(am - vdA[k] * LOG2E + vlt[k]) : 0.f;
+              const float w1 = (k + 1 <= m && k + 1 < len) ? cbv.y * exp2f(am - vdA[k + 1] * LOG2E + vlt[k + 1]) : 0.f;
+              v[e] = pack2rn<BF16>(w0, w1);
+            }
+          }
+          st_shared_v4(row + q * 16, v[0], v[1], v[2], v[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_built(2 * bi + kh));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_vec_empty(vb));
+    }
+  } else if (warp >= 12) {
+    // ===== epilogue: out[m][p] = exp(dA[m]) O1 + O2 + D x  (TMEM lane m of each row tile) =====
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    int lu = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      int b, c, h;
+      decode(u, b, c, h);
+      const int a = lu & 1;
+      const int vb = lu & 1;
+      const float Dh = p.D ? p.D[h] : 0.f;
+      mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
+      const float* vdA = vec + vb * 2 * Q;
+      mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int m = mt * 128 + r;
+        const int t = c * Q + m;
+        const float sm = exp2f(vdA[m] * LOG2E);
+        const uint32_t tacc = tmem_base + lane_off + a * 256 + 128 * mt;
+        const size_t ro = (((size_t)b * p.L + t) * p.H + h) * P;  // element offset of row t
+        const bool ok = t < p.L;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t o1[32], o2[32];
+          tmem_ld32(tacc + cc * 32, o1);
+          tmem_ld32(tacc + 64 + cc * 32, o2);
+          tmem_ld_wait();
+          if (ok) {
+            const uint4* xs = reinterpret_cast<const uint4*>(
+                reinterpret_cast<const uint8_t*>(p.x) + (ro + cc * 32) * 2);
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 xv = __ldg(xs + q);
+              const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 xf = unpack2<BF16>(xw[e]);
+                const int j = 8 * q + 2 * e;
+                const float y0 = sm * __uint_as_float(o1[j]) + __uint_as_float(o2[j]) + Dh * xf.x;
+                const float y1 = sm * __uint_as_float(o1[j + 1]) + __uint_as_float(o2[j + 1]) + Dh * xf.y;
+                pk[4 * q + e] = pack2rn<BF16>(y0, y1);
+              }
+            }
+            uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) + (ro + cc * 32) * 2;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4(dst + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(bar_acc_empty(a));
+        mbar_arrive(bar_vec_empty(vb));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+}  // namespace ssd
+}  // namespace tlattn

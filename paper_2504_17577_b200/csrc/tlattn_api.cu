@@ -22,6 +22,7 @@
 #include "gemm_sm100_2sm.cuh"
 #include "gemv_sm100.cuh"
 #include "mla_decode_sm100.cuh"
+#include "ssd_sm100.cuh"
 
 using namespace tlattn;
 
@@ -62,7 +63,7 @@ struct DeviceInfo {
   int major = 0, minor = 0;
   bool ok = false;
   // per kernel instantiation: cudaFuncAttributeMaxDynamicSharedMemorySize already set.
-  // Slots: attention 0-7, replicated-output attention 8-15, GEMM 16-17.
+  // Slots: attention 0-7, replicated-output attention 8-15, GEMM 16-17, SSD 18-21.
   bool smem_set[32] = {};
 };
 
@@ -918,6 +919,138 @@ extern "C" int tl_mla_decode(const void* q, const void* q_pe, const void* kv, co
   else
     rc = bf ? launch_mla<32, true>(prm, dev, B, seqlens, Skv, st) : launch_mla<32, false>(prm, dev, B, seqlens, Skv, st);
   if (rc == TL_OK) g_last_launches = 3;
+  return rc;
+}
+
+// ------------------------------------------------------------------ SSD chunk kernels (N4)
+namespace {
+int ssd_validate(int batch, int seqlen, int nheads, int ngroups, int headdim, int dstate,
+                 int chunk_size, int dtype) {
+  if (batch < 1 || seqlen < 1 || nheads < 1 || ngroups < 1 || headdim < 1 || dstate < 1 ||
+      chunk_size < 1)
+    return TL_ERR_INVALID_VALUE;
+  if (nheads % ngroups != 0) return TL_ERR_INVALID_VALUE;
+  if (dtype != TL_DTYPE_F16 && dtype != TL_DTYPE_BF16) return TL_ERR_INVALID_VALUE;
+  if (headdim != ssd::P || dstate != ssd::N || chunk_size != ssd::Q) return TL_ERR_UNSUPPORTED;
+  const long long nc = (seqlen + (long long)chunk_size - 1) / chunk_size;
+  if ((long long)batch * nc > 0x7fffffffLL || (long long)batch * nc * nheads > 0x7fffffffLL)
+    return TL_ERR_UNSUPPORTED;
+  return TL_OK;
+}
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool al4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) == 0; }
+
+template <class K>
+int ssd_launch(K kern, int smem, int threads, const ssd::SsdParams& prm, DeviceInfo& di, int inst,
+               cudaStream_t stream) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di.smem_set[inst]) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return TL_ERR_CUDA;
+      }
+      di.smem_set[inst] = true;
+    }
+  }
+  const int grid = prm.n_units < di.sm_count ? prm.n_units : di.sm_count;
+  kern<<<grid, threads, smem, stream>>>(prm);
+  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  return TL_OK;
+}
+}  // namespace
+
+extern "C" int tl_ssd_chunk_state(const void* x, const void* Bm, const float* dt, const float* dA,
+                                  void* states, int batch, int seqlen, int nheads, int ngroups,
+                                  int headdim, int dstate, int chunk_size, int dtype,
+                                  void* stream) {
+  g_last_launches = 0;
+  if (!x || !Bm || !dt || !dA || !states) return TL_ERR_INVALID_VALUE;
+  int rc = ssd_validate(batch, seqlen, nheads, ngroups, headdim, dstate, chunk_size, dtype);
+  if (rc != TL_OK) return rc;
+  // head pairs share a CTA and its Bm tile: both heads of a pair must be in one group
+  if (nheads % 2 != 0 || (nheads / ngroups) % 2 != 0) return TL_ERR_UNSUPPORTED;
+  if (!al16(x) || !al16(Bm) || !al16(states) || !al4(dt) || !al4(dA)) return TL_ERR_UNSUPPORTED;
+  int dev;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  ssd::SsdParams prm;
+  std::memset(&prm, 0, sizeof prm);
+  const cuuint64_t L = seqlen, Bn = batch;
+  if (!encode_4d_cached(enc, &prm.tm_x, x, dtype, {(cuuint64_t)ssd::P, (cuuint64_t)nheads, L, Bn},
+                        {64, 1, 64, 1}) ||
+      !encode_4d_cached(enc, &prm.tm_b, Bm, dtype, {(cuuint64_t)ssd::N, (cuuint64_t)ngroups, L, Bn},
+                        {64, 1, 64, 1}))
+    return TL_ERR_CUDA;
+  prm.dt = dt;
+  prm.dA = dA;
+  prm.out = states;
+  prm.B = batch;
+  prm.L = seqlen;
+  prm.H = nheads;
+  prm.G = ngroups;
+  prm.nc = (seqlen + chunk_size - 1) / chunk_size;
+  prm.grp = nheads / ngroups;
+  prm.n_units = batch * prm.nc * (nheads / 2);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rc = dtype == TL_DTYPE_BF16
+           ? ssd_launch(ssd::tl_ssd_state_kernel<true>, ssd::StateCfg::SMEM_BYTES, ssd::StateCfg::THREADS, prm, *di, 18, st)
+           : ssd_launch(ssd::tl_ssd_state_kernel<false>, ssd::StateCfg::SMEM_BYTES, ssd::StateCfg::THREADS, prm, *di, 19, st);
+  if (rc == TL_OK) g_last_launches = 1;
+  return rc;
+}
+
+extern "C" int tl_ssd_chunk_scan(const void* cb, const void* x, const float* dt, const float* dA,
+                                 const void* C, const void* prev_states, const float* D, void* out,
+                                 int batch, int seqlen, int nheads, int ngroups, int headdim,
+                                 int dstate, int chunk_size, int dtype, void* stream) {
+  g_last_launches = 0;
+  if (!cb || !x || !dt || !dA || !C || !prev_states || !out) return TL_ERR_INVALID_VALUE;
+  int rc = ssd_validate(batch, seqlen, nheads, ngroups, headdim, dstate, chunk_size, dtype);
+  if (rc != TL_OK) return rc;
+  if (!al16(cb) || !al16(x) || !al16(C) || !al16(prev_states) || !al16(out) || !al4(dt) ||
+      !al4(dA) || (D && !al4(D)))
+    return TL_ERR_UNSUPPORTED;
+  int dev;
+  DeviceInfo* di;
+  if ((rc = current_device(&dev, &di)) != TL_OK) return rc;
+  auto enc = get_encode();
+  if (!enc) return TL_ERR_CUDA;
+  ssd::SsdParams prm;
+  std::memset(&prm, 0, sizeof prm);
+  const int nc = (seqlen + chunk_size - 1) / chunk_size;
+  const cuuint64_t L = seqlen, Bn = batch, BNC = (cuuint64_t)batch * nc;
+  if (!encode_4d_cached(enc, &prm.tm_x, x, dtype, {(cuuint64_t)ssd::P, (cuuint64_t)nheads, L, Bn},
+                        {64, 1, 128, 1}) ||
+      !encode_4d_cached(enc, &prm.tm_c, C, dtype, {(cuuint64_t)ssd::N, (cuuint64_t)ngroups, L, Bn},
+                        {64, 1, 128, 1}) ||
+      !encode_4d_cached(enc, &prm.tm_cb, cb, dtype,
+                        {(cuuint64_t)ssd::Q, (cuuint64_t)ssd::Q, (cuuint64_t)ngroups, BNC},
+                        {64, 128, 1, 1}) ||
+      !encode_4d_cached(enc, &prm.tm_s, prev_states, dtype,
+                        {(cuuint64_t)ssd::N, (cuuint64_t)ssd::P, (cuuint64_t)nheads, BNC},
+                        {64, 64, 1, 1}))
+    return TL_ERR_CUDA;
+  prm.dt = dt;
+  prm.dA = dA;
+  prm.D = D;
+  prm.x = x;
+  prm.out = out;
+  prm.B = batch;
+  prm.L = seqlen;
+  prm.H = nheads;
+  prm.G = ngroups;
+  prm.nc = nc;
+  prm.grp = nheads / ngroups;
+  prm.n_units = batch * nc * nheads;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  rc = dtype == TL_DTYPE_BF16
+           ? ssd_launch(ssd::tl_ssd_scan_kernel<true>, ssd::ScanCfg::SMEM_BYTES, ssd::ScanCfg::THREADS, prm, *di, 20, st)
+           : ssd_launch(ssd::tl_ssd_scan_kernel<false>, ssd::ScanCfg::SMEM_BYTES, ssd::ScanCfg::THREADS, prm, *di, 21, st);
+  if (rc == TL_OK) g_last_launches = 1;
   return rc;
 }
 

@@ -73,6 +73,10 @@ def load_library(path: str | None = None):
         lib.tl_peer_barrier_set_timeout_ns.restype = I
         lib.tl_peer_barrier_check.argtypes = [P]
         lib.tl_peer_barrier_check.restype = I
+        lib.tl_ssd_chunk_state.argtypes = [P, P, P, P, P, I, I, I, I, I, I, I, I, P]
+        lib.tl_ssd_chunk_state.restype = I
+        lib.tl_ssd_chunk_scan.argtypes = [P, P, P, P, P, P, P, P, I, I, I, I, I, I, I, I, P]
+        lib.tl_ssd_chunk_scan.restype = I
         lib.tl_attn_set_option.argtypes = [I, I]
         lib.tl_attn_set_option.restype = I
         lib.tl_attn_get_option.argtypes = [I]
@@ -389,3 +393,72 @@ class HostAttention:
         tl_attn_fwd_host(q_h, k_h, v_h, o_h, lse_h if self.with_lse else None, B, Hq, Hkv, Sq,
                          Skv, D, int(bool(causal)), scale, dtype_code(q_h.dtype), self.ws,
                          self.ws_bytes, stream)
+
+
+# --------------------------------------------------------------------------- Mamba-2 SSD
+def tl_ssd_chunk_state(x, Bm, dt, dA, states, batch, seqlen, nheads, ngroups, headdim, dstate,
+                       chunk_size, dtype, stream=None):
+    """Direct mirror of the C entry point (Table 4; include/tlattn.h)."""
+    _check(load_library().tl_ssd_chunk_state(
+        _ptr(x), _ptr(Bm), _ptr(dt), _ptr(dA), _ptr(states), int(batch), int(seqlen), int(nheads),
+        int(ngroups), int(headdim), int(dstate), int(chunk_size), int(dtype), _stream_handle(stream)))
+
+
+def tl_ssd_chunk_scan(cb, x, dt, dA, C, prev_states, D, out, batch, seqlen, nheads, ngroups,
+                      headdim, dstate, chunk_size, dtype, stream=None):
+    """Direct mirror of the C entry point (Table 4; include/tlattn.h)."""
+    _check(load_library().tl_ssd_chunk_scan(
+        _ptr(cb), _ptr(x), _ptr(dt), _ptr(dA), _ptr(C), _ptr(prev_states), _ptr(D), _ptr(out),
+        int(batch), int(seqlen), int(nheads), int(ngroups), int(headdim), int(dstate),
+        int(chunk_size), int(dtype), _stream_handle(stream)))
+
+
+def _ssd_dims(x, BC, dt, dA, chunk_size):
+    if x.dim() != 4 or BC.dim() != 4 or dt.dim() != 4 or dA.shape != dt.shape:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "expected x[B,L,H,P], B/C[B,L,G,N], "
+                          "dt/dA[B,H,nchunks,Q]")
+    Bn, L, H, P = x.shape
+    G, N = BC.shape[2], BC.shape[3]
+    nc = (L + chunk_size - 1) // chunk_size
+    if tuple(BC.shape[:2]) != (Bn, L) or tuple(dt.shape) != (Bn, H, nc, chunk_size):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "SSD input shapes disagree")
+    if dt.dtype != torch.float32 or dA.dtype != torch.float32 or BC.dtype != x.dtype:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "dt / dA must be fp32, x / B / C one 16-bit dtype")
+    for t in (x, BC, dt, dA):
+        if not (t.is_cuda and t.is_contiguous() and t.device == x.device):
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "SSD inputs must be contiguous CUDA tensors "
+                              "on one device")
+    return Bn, L, H, G, P, N, nc
+
+
+def ssd_chunk_state(x, Bm, dt, dA, chunk_size=256, out=None, stream=None):
+    """states[B,nchunks,H,P,N] of Mamba-2's chunk_state on the GPU (allocates the output)."""
+    Bn, L, H, G, P, N, nc = _ssd_dims(x, Bm, dt, dA, chunk_size)
+    shape = (Bn, nc, H, P, N)
+    if out is not None:
+        _check_out(out, shape, x.dtype, x.device, "out")
+    st = out if out is not None else torch.empty(shape, dtype=x.dtype, device=x.device)
+    tl_ssd_chunk_state(x, Bm, dt, dA, st, Bn, L, H, G, P, N, chunk_size, dtype_code(x.dtype),
+                       stream)
+    return st
+
+
+def ssd_chunk_scan(cb, x, dt, dA, C, prev_states, D=None, chunk_size=256, out=None, stream=None):
+    """out[B,L,H,P] of Mamba-2's chunk_scan on the GPU (allocates the output)."""
+    Bn, L, H, G, P, N, nc = _ssd_dims(x, C, dt, dA, chunk_size)
+    if tuple(cb.shape) != (Bn, nc, G, chunk_size, chunk_size) or cb.dtype != x.dtype:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "cb must be [B,nchunks,G,Q,Q] in x's dtype")
+    if tuple(prev_states.shape) != (Bn, nc, H, P, N) or prev_states.dtype != x.dtype:
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "prev_states must be [B,nchunks,H,P,N] in x's dtype")
+    if D is not None and (tuple(D.shape) != (H,) or D.dtype != torch.float32):
+        raise TlAttnError(TL_ERR_INVALID_VALUE, "D must be fp32 [H]")
+    for t in (cb, prev_states, D):
+        if t is not None and not (t.is_cuda and t.is_contiguous() and t.device == x.device):
+            raise TlAttnError(TL_ERR_INVALID_VALUE, "SSD inputs must be contiguous CUDA tensors "
+                              "on one device")
+    if out is not None:
+        _check_out(out, x.shape, x.dtype, x.device, "out")
+    o = out if out is not None else torch.empty_like(x)
+    tl_ssd_chunk_scan(cb, x, dt, dA, C, prev_states, D, o, Bn, L, H, G, P, N, chunk_size,
+                      dtype_code(x.dtype), stream)
+    return o
