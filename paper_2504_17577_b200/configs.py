@@ -158,3 +158,59 @@ MLA_CONFIGS = [
     MlaConfig("MLA3", 32, 128, 1, 16384, torch.bfloat16, True, 2003,
               note="ragged cache lengths uniform in [1, 16384]"),
 ]
+
+
+@dataclass(frozen=True)
+class SsdConfig:
+    """Mamba-2 SSD chunk kernels on the paper's Table 4 shapes:
+    CC<i> = chunk_scan, CT<i> = chunk_state; nheads 64, head_dim 64, d_state 128; chunk
+    length 256 and one group (readings L2, L3); bf16 (reading L8)."""
+    name: str
+    kind: str  # "scan" | "state"
+    B: int
+    L: int
+    H: int = 64
+    G: int = 1
+    P: int = 64
+    N: int = 128
+    Q: int = 256
+    dtype: torch.dtype = torch.bfloat16
+    seed: int = 4000
+
+    @property
+    def nc(self) -> int:
+        return (self.L + self.Q - 1) // self.Q
+
+    def flops(self) -> float:
+        """Multiply-adds x 2 of the definition: state 2 B nc H P N Q; scan 2 B L H P N
+        (entering state) + 2 B H P sum_i (i + 1) per chunk (causal intra-chunk sum)."""
+        if self.kind == "state":
+            return 2.0 * self.B * self.nc * self.H * self.P * self.N * self.Q
+        intra = sum(min(self.Q, self.L - c * self.Q) * (min(self.Q, self.L - c * self.Q) + 1) / 2
+                    for c in range(self.nc))
+        return 2.0 * self.B * self.L * self.H * self.P * self.N + 2.0 * self.B * self.H * self.P * intra
+
+    def hbm_bytes(self) -> float:
+        """Algorithmic HBM bytes: every input read once, the output written once."""
+        e = 2
+        x = e * self.B * self.L * self.H * self.P
+        bc = e * self.B * self.L * self.G * self.N
+        vec = 2 * 4 * self.B * self.H * self.nc * self.Q                 # dt, dA (fp32)
+        states = e * self.B * self.nc * self.H * self.P * self.N
+        if self.kind == "state":
+            return x + bc + vec + states
+        cb = e * self.B * self.nc * self.G * self.Q * self.Q
+        return cb + x + bc + vec + states + x + 4 * self.H                # + out, D
+
+    def as_dict(self):
+        return {"workload": self.name, "kind": self.kind, "batch": self.B, "seqlen": self.L,
+                "nheads": self.H, "ngroups": self.G, "headdim": self.P, "dstate": self.N,
+                "chunk_size": self.Q, "dtype": {torch.float16: "f16", torch.bfloat16: "bf16"}[self.dtype]}
+
+
+_T4 = {"0": (1, 1024), "1": (1, 2048), "2": (1, 8192), "3": (64, 1024), "4": (64, 2048),
+       "5": (64, 8192)}
+SSD_CONFIGS = {}
+for _i, (_b, _l) in _T4.items():
+    SSD_CONFIGS["CC" + _i] = SsdConfig("CC" + _i, "scan", _b, _l, seed=4000 + int(_i))
+    SSD_CONFIGS["CT" + _i] = SsdConfig("CT" + _i, "state", _b, _l, seed=4100 + int(_i))

@@ -22,9 +22,12 @@
 //     so the Bm tile of a chunk is read from HBM once and from L2 by the other head pairs.
 //   * chunk_scan unit = (b, c, h), two M = 128 row tiles: O1 = C [m][n] . prev [p][n]^T
 //     (both K-major, K = n = 128), O2 = W [m][k] . x [k][p] (x MN-major, K = k) with
-//     W = cb . exp(dA[m] - dA[k]) dt[k] . [k <= m] built in SMEM over the cb tile by eight
-//     "W" warps (one row per thread, two threads per row: 64 k each); the causal structure
-//     skips the (m0, k1) block. The epilogue warps form out = exp(dA[m]) O1 + O2 + D x.
+//     the decay split per MMA K step of 16 keys: exp(dA_m - dA_k) dt_k =
+//     exp2(a_m - a_{k0(k)}) * [dt_k exp2(a_{k0(k)} - a_k)] with a = dA log2 e; the second
+//     (bounded) factor scales the x rows, the first (one exp per row and K step) the cb tile:
+//     W = cb exp2(a_m - a_k0) [k <= m], built in SMEM by 16 "W" warps (one row per thread,
+//     four threads per row: 32 keys each); the causal structure skips the (m0, k1) block.
+//     The epilogue warps form out = exp(dA[m]) O1 + O2 + D x.
 //   * every operand streams through one ring of 16 KB TMA slots (per-slot full / empty
 //     barriers; the six W half-blocks of a unit also have "built" barriers) in one fixed
 //     per-unit order that the producer, W warps and MMA warp all follow.
@@ -59,7 +62,19 @@ struct SsdParams {
   void* out;          // states [B][nc][H][P][N] (state) / out [B][L][H][P] (scan)
   int B, L, H, G, nc, grp;  // grp = H / G
   int n_units;
+  unsigned long long* trace;  // debug builds (TLATTN_TRACE) only: event clocks of CTA 0
 };
+
+#ifdef TLATTN_TRACE
+#define SSD_TRACE(idx)                                                                 \
+  do {                                                                                 \
+    if (p.trace != nullptr && blockIdx.x == 0 && (idx) < 4000) p.trace[(idx)] = clock64(); \
+  } while (0)
+#else
+#define SSD_TRACE(idx) \
+  do {                 \
+  } while (0)
+#endif
 
 template <bool BF16>
 __device__ __forceinline__ float2 unpack2(uint32_t v) {
@@ -160,6 +175,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
           const int s = it % C::NST;
           if (it >= C::NST) mbar_wait(bar_empty(s), ((it / C::NST) - 1) & 1);
           mbar_arrive_expect_tx(bar_full(s), 2 * SLOT);
+          SSD_TRACE(it * 4 + 0);
           const uint32_t dst = sRing + s * 2 * SLOT;
           const int t0 = c * Q + st * 64;
           // x rows [t0, t0+64) of heads h0, h0+1 (OOB rows past L zero-filled), then Bm
@@ -185,6 +201,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       for (int st = 0; st < C::STAGES; ++st, ++it) {
         const int s = it % C::NST;
         mbar_wait(bar_scaled(s), (it / C::NST) & 1);
+        if (lane == 0) SSD_TRACE(it * 4 + 2);
         tc_fence_after();
         const uint32_t xa = sRing + s * 2 * SLOT;
 #pragma unroll
@@ -202,36 +219,59 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
     // ===== scale warps: x row (t, head) *= w[t] = exp(dA[last] - dA[t]) dt[t], in SMEM =====
     const int i = threadIdx.x - 128;
     const int r = i & 63, hh = i >> 6;
-    int it = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    // this thread's decay inputs of a unit: dA[last], and dA / dt at its row of each stage;
+    // loaded one unit ahead so the global-load latency is off the per-stage path
+    struct Raw {
+      float last, dA[C::STAGES], dt[C::STAGES];
+      int len;
+    };
+    auto load_raw = [&](int u) {
+      Raw v;
       int b, c, hp;
       decode(u, b, c, hp);
       const int h = 2 * hp + hh;
-      const int len = min(Q, p.L - c * Q);
+      v.len = min(Q, p.L - c * Q);
       const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
-      const float dA_last = p.dA[vo + len - 1];
+      v.last = __ldg(p.dA + vo + v.len - 1);
+#pragma unroll
+      for (int st = 0; st < C::STAGES; ++st) {
+        v.dA[st] = __ldg(p.dA + vo + st * 64 + r);
+        v.dt[st] = __ldg(p.dt + vo + st * 64 + r);
+      }
+      return v;
+    };
+    int it = 0;
+    Raw cur = load_raw(blockIdx.x < p.n_units ? blockIdx.x : 0);
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const int un = u + gridDim.x;
+      const Raw nxt = load_raw(un < p.n_units ? un : u);
       for (int st = 0; st < C::STAGES; ++st, ++it) {
         const int s = it % C::NST;
         const int pos = st * 64 + r;
-        const float w = pos < len ? exp2f((dA_last - p.dA[vo + pos]) * LOG2E) * p.dt[vo + pos] : 0.f;
+        const float w = pos < cur.len ? ex2((cur.last - cur.dA[st]) * LOG2E) * cur.dt[st] : 0.f;
         mbar_wait(bar_full(s), (it / C::NST) & 1);
-        // row r of box hh: 128 B (a SW128 row stays one row; only its 16-B units permute)
+        if (i == 0) SSD_TRACE(it * 4 + 1);
+        // row r of box hh: 128 B (a SW128 row stays one row; only its 16-B units permute).
+        // Thread r walks the units starting at r & 7, so the 8 threads of a quarter-warp
+        // (rows r..r+7, 128 B apart) hit 8 different bank groups (no 8-way conflict).
         const uint32_t row = sRing + s * 2 * SLOT + hh * 8192 + r * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
+          const uint32_t addr = row + ((q ^ (r & 7)) << 4);
           uint32_t v[4];
-          ld_shared_v4(row + q * 16, v);
+          ld_shared_v4(addr, v);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = unpack2<BF16>(v[e]);
             v[e] = pack2rn<BF16>(f.x * w, f.y * w);
           }
-          st_shared_v4(row + q * 16, v[0], v[1], v[2], v[3]);
+          st_shared_v4(addr, v[0], v[1], v[2], v[3]);
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_scaled(s));
       }
+      cur = nxt;
     }
   } else if (warp >= 8) {
     // ===== epilogue: TMEM lane m = (head h0 + m/64, p = m%64) -> 128 states, RN, global =====
@@ -245,6 +285,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       const int a = lu & 1;
       const int h = 2 * hp + (m >> 6), pp = m & 63;
       mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
+      if (m == 0) SSD_TRACE(2000 + lu * 2);
       tc_fence_after();
       uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) +
                      ((((size_t)b * p.nc + c) * p.H + h) * P + pp) * (size_t)N * 2;
@@ -263,6 +304,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       }
       tc_fence_before();
       __syncwarp();
+      if (m == 0) SSD_TRACE(2000 + lu * 2 + 1);
       if (lane == 0) mbar_arrive(bar_acc_empty(a));
     }
   }
@@ -276,23 +318,29 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
 
 // ============================================================================ chunk_scan
 // Per-unit ring items (16 KB slots), in the order the MMA consumes them:
-//   0 S (prev [64 p][128 n], 2 boxes) | 1-2 C rows 0-127 (n halves) | 3 x rows 0-127 |
-//   4-5 cb (m 0-127, k 0-127: k halves) | 6-7 C rows 128-255 | 8-9 cb (m 128-255, k 0-127) |
+//   0 S (prev [64 p][128 n], 2 boxes) | 1-2 C rows 0-127 (n halves) | 3-4 C rows 128-255 |
+//   5 x rows 0-127 | 6-7 cb (m 0-127, k 0-127: k halves) | 8-9 cb (m 128-255, k 0-127) |
 //   10 x rows 128-255 | 11-12 cb (m 128-255, k 128-255)
+// Both C . prev GEMMs run first, so the slots free up in about the order they were filled
+// and the next unit's S and C stream in while this unit's W blocks are still being used.
 struct ScanCfg {
   static constexpr int NSLOT = 12;
   static constexpr int ITEMS = 13;
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // dA, log2 dt of the unit: 2 x Q f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * Q * 4;   // double-buffered over units
-  // full[NSLOT] empty[NSLOT] built[6] acc_full[2] acc_empty[2] vec_full[2] vec_empty[2].
+  // full[NSLOT] empty[NSLOT] built[6] acc_full[2] acc_empty[2] vec_full[2] vec_empty[2]
+  // xsc[2] (x rows k-tile 0 / 1 scaled by xs).
   // built[2 * block + k half] completes once per unit (W blocks (m0,k0) (m1,k0) (m1,k1)):
   // a per-slot "built" barrier would complete only on the slot's W fills and fall out of
   // step with the fill count that the waiters' parity follows.
-  static constexpr int NUM_BARS = 2 * NSLOT + 6 + 8;
+  static constexpr int NUM_BARS = 2 * NSLOT + 6 + 8 + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
-  static constexpr int THREADS = 512;  // 0 TMA, 1 MMA, 2 vectors, 4-11 W builders, 12-15 epilogue
+  // warps: 0 TMA, 1 MMA, 2 unit vectors, 4-19 W builders (4 key quarters x 4 lane
+  // quarters), 20-23 epilogue
+  static constexpr int THREADS = 24 * 32;
+  static constexpr int W_WARP0 = 4, EPI_WARP0 = 20;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
 };
 
@@ -304,7 +352,8 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   const uint32_t base = smem_u32(smem_raw);
   if ((base & 1023u) != 0u) __trap();
   const uint32_t sRing = base + C::OFF_RING;
-  float* vec = reinterpret_cast<float*>(smem_raw + C::OFF_VEC);  // [buf][dA | log2 dt][Q]
+  // [buf][a_i = dA_i log2 e | xs_i = dt_i exp2(a_{k0(i)} - a_i)][Q] (see the vector warp)
+  float* vec = reinterpret_cast<float*>(smem_raw + C::OFF_VEC);
   const uint32_t bar0 = base + C::OFF_BAR;
   auto bar_full = [&](int s) { return bar0 + 8u * s; };
   auto bar_empty = [&](int s) { return bar0 + 8u * (C::NSLOT + s); };
@@ -313,6 +362,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   auto bar_acc_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + i); };
   auto bar_vec_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 10 + i); };
   auto bar_vec_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 12 + i); };
+  auto bar_xsc = [&](int kt) { return bar0 + 8u * (2 * C::NSLOT + 14 + kt); };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -326,12 +376,13 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       mbar_init(bar_full(s), 1);
       mbar_init(bar_empty(s), 1);
     }
-    for (int w = 0; w < 6; ++w) mbar_init(bar_built(w), 4);  // the 4 W warps of one k half
+    for (int w = 0; w < 6; ++w) mbar_init(bar_built(w), 8);  // the 8 W warps of one k half
+    for (int kt = 0; kt < 2; ++kt) mbar_init(bar_xsc(kt), 4);  // one W lane-quarter group
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_acc_full(i), 1);
       mbar_init(bar_acc_empty(i), 4);
       mbar_init(bar_vec_full(i), 1);
-      mbar_init(bar_vec_empty(i), 8 + 4);  // W warps + epilogue warps
+      mbar_init(bar_vec_empty(i), 16 + 4);  // W warps + epilogue warps
     }
     fence_mbar_init();
   }
@@ -364,6 +415,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
           const int s = f % C::NSLOT;
           if (f >= C::NSLOT) mbar_wait(bar_empty(s), ((f / C::NSLOT) - 1) & 1);
           mbar_arrive_expect_tx(bar_full(s), SLOT);
+          if (f < 260) SSD_TRACE(f);  // item f's TMA issued (its slot was free)
           const uint32_t dst = sRing + s * SLOT;
           const uint32_t fb = bar_full(s);
           switch (item) {
@@ -371,19 +423,19 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
               tma_load_4d(dst, &p.tm_s, fb, 0, 0, h, bc, pol_s);
               tma_load_4d(dst + 8192, &p.tm_s, fb, 64, 0, h, bc, pol_s);
               break;
-            case 1: case 2: case 6: case 7: {  // C [128 t][64 n] (n half, row tile)
-              const int mt = item >= 6, nh = (item - (mt ? 6 : 1));
+            case 1: case 2: case 3: case 4: {  // C [128 t][64 n] (row tile, n half)
+              const int mt = item >= 3, nh = (item - 1) & 1;
               tma_load_4d(dst, &p.tm_c, fb, 64 * nh, g, c * Q + 128 * mt, b, pol_l);
               break;
             }
-            case 3: case 10: {  // x [128 k][64 p]
+            case 5: case 10: {  // x [128 k][64 p]
               const int kt = item == 10;
               tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * kt, b, pol_s);
               break;
             }
-            default: {  // cb [128 m][64 k]: items 4,5 (m0 k0), 8,9 (m1 k0), 11,12 (m1 k1)
+            default: {  // cb [128 m][64 k]: items 6,7 (m0 k0), 8,9 (m1 k0), 11,12 (m1 k1)
               const int mt = item >= 8, kt = item >= 11;
-              const int kh = (item == 5 || item == 9 || item == 12);
+              const int kh = (item == 7 || item == 9 || item == 12);
               tma_load_4d(dst, &p.tm_cb, fb, 128 * kt + 64 * kh, 128 * mt, g, bc, pol_l);
               break;
             }
@@ -424,7 +476,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       // O2[mt] += W[mt][kt] . x[kt]: A items (wa, wb) = k halves of W block wblk (built),
       // B = x item
       auto gemm2 = [&](int mt, int wblk, int wa, int wb, int xi, bool first) {
-        mbar_wait(bar_full(slot(xi)), par(xi));
+        mbar_wait(bar_xsc(xi == 10), lu & 1);  // x~ = xs * x rows of this k-tile
         mbar_wait(bar_built(2 * wblk), lu & 1);
         mbar_wait(bar_built(2 * wblk + 1), lu & 1);
         tc_fence_after();
@@ -440,21 +492,32 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       auto release = [&](int item) {
         if (elect_one()) mma_commit(bar_empty(slot(item)));
       };
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 0);  // unit start (acc free)
       gemm1(0, 1, 2);
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 1);
       release(1), release(2);
-      gemm2(0, 0, 4, 5, 3, true);
-      release(4), release(5);
-      gemm1(1, 6, 7);
-      release(0), release(6), release(7);
-      gemm2(1, 1, 8, 9, 3, true);
-      release(3), release(8), release(9);
+      gemm1(1, 3, 4);
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 2);
+      release(0), release(3), release(4);
+      gemm2(0, 0, 6, 7, 5, true);
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 3);
+      release(6), release(7);
+      gemm2(1, 1, 8, 9, 5, true);
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 4);
+      release(5), release(8), release(9);
       gemm2(1, 2, 11, 12, 10, false);
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 5);
       release(10), release(11), release(12);
       if (elect_one()) mma_commit(bar_acc_full(a));
     }
     __syncwarp();
   } else if (warp == 2) {
-    // ====== unit vectors: dA and log2(dt) of (b, h, c) into SMEM (double-buffered) ======
+    // ====== unit vectors of (b, h, c) into SMEM (double-buffered):
+    //   a_i  = dA_i log2 e
+    //   xs_i = dt_i exp2(a_{k0(i)} - a_i), k0(i) = 16 floor(i / 16) (the MMA K step of i)
+    // so that exp(dA_m - dA_k) dt_k = exp2(a_m - a_{k0(k)}) * xs_k: the first factor is
+    // one exp per (row, K step) applied to cb, the second a per-row scale of x (bounded:
+    // at most 16 positions of decay, <= 2^37 at the Mamba-2 initialisation ranges) ======
     int lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
       int b, c, h;
@@ -464,17 +527,21 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
       float* dst = vec + vb * 2 * Q;
       for (int i = lane; i < Q; i += 32) {
-        dst[i] = p.dA[vo + i];
-        dst[Q + i] = __log2f(p.dt[vo + i]);
+        const float a = __ldg(p.dA + vo + i) * LOG2E;
+        const float a0 = __ldg(p.dA + vo + (i & ~15)) * LOG2E;
+        dst[i] = a;
+        dst[Q + i] = __ldg(p.dt + vo + i) * ex2(a0 - a);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_vec_full(vb));  // release: smem writes visible to waiters
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ===== W builders: row m of a cb block, k half kh: W = cb exp2((dA[m]-dA[k]) log2e + log2 dt[k]) [k <= m, k < len]
+  } else if (warp >= C::W_WARP0 && warp < C::EPI_WARP0) {
+    // ===== W builders: row r of a cb block, 32 keys per thread (key quarter kq):
+    //       W[m][k] = cb[m][k] exp2(a_m + c_k) for k <= m and k < len, else 0 =====
     const int q4 = warp & 3;
-    const int kh = (warp - 4) >> 2;  // k half of each cb block this warp builds
-    const int r = q4 * 32 + lane;    // row within the 128-row tile
+    const int kq = (warp - C::W_WARP0) >> 2;  // key quarter of each 128-key block
+    const int kh = kq >> 1;                   // the slot (64-key half) it lies in
+    const int r = q4 * 32 + lane;             // row within the 128-row tile
     int f = 0, lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu, f += C::ITEMS) {
       int b, c, h;
@@ -482,47 +549,88 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       const int len = min(Q, p.L - c * Q);
       const int vb = lu & 1;
       mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
-      const float* vdA = vec + vb * 2 * Q;
-      const float* vlt = vdA + Q;
-      // blocks (mt, kt, item of this warp's k half)
-      const int blk_mt[3] = {0, 1, 1}, blk_kt[3] = {0, 0, 1};
-      const int blk_it[3] = {4 + kh, 8 + kh, 11 + kh};
-#pragma unroll
-      for (int bi = 0; bi < 3; ++bi) {
-        const int item = blk_it[bi];
+      const float* va = vec + vb * 2 * Q;
+      const float* vxs = va + Q;
+      // x rows of k-tile kt: x~[k][p] = xs_k x[k][p] in place (row r = key r of the tile; a
+      // SW128 row stays a row, the walk starts at unit r & 7: no bank conflicts). k-tile 0
+      // (needed by the first W.x GEMM) is scaled by key quarter 0 before its W blocks,
+      // k-tile 1 (only the last GEMM) by key quarter 1 after its second block.
+      auto scale_x = [&](int kt) {
+        const int item = kt ? 10 : 5;
         const int s = (f + item) % C::NSLOT;
         mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
-        const int m = blk_mt[bi] * 128 + r;             // row within the chunk
-        const int k0 = blk_kt[bi] * 128 + 64 * kh;     // first key (column) of this half
-        const float am = vdA[min(m, Q - 1)] * LOG2E;
+        const int k = kt * 128 + r;
+        const float w = k < len ? vxs[k] : 0.f;
         const uint32_t row = sRing + s * SLOT + r * 128;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // 16-B unit q of the row holds keys 8 (q ^ (r & 7)) ..
-          const int kb = k0 + 8 * (q ^ (r & 7));
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t addr = row + ((q ^ (r & 7)) << 4);
           uint32_t v[4];
-          if (kb > m || kb >= len) {  // the whole unit is masked (above the diagonal / past len)
-            v[0] = v[1] = v[2] = v[3] = 0u;
-          } else {
-            ld_shared_v4(row + q * 16, v);
+          ld_shared_v4(addr, v);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int k = kb + 2 * e;
-              const float2 cbv = unpack2<BF16>(v[e]);
-              const float w0 = (k <= m && k < len) ? cbv.x * exp2f(am - vdA[k] * LOG2E + vlt[k]) : 0.f;
-              const float w1 = (k + 1 <= m && k + 1 < len) ? cbv.y * exp2f(am - vdA[k + 1] * LOG2E + vlt[k + 1]) : 0.f;
-              v[e] = pack2rn<BF16>(w0, w1);
-            }
+          for (int e = 0; e < 4; ++e) {
+            const float2 xf = unpack2<BF16>(v[e]);
+            v[e] = pack2rn<BF16>(xf.x * w, xf.y * w);
           }
-          st_shared_v4(row + q * 16, v[0], v[1], v[2], v[3]);
+          st_shared_v4(addr, v[0], v[1], v[2], v[3]);
         }
         fence_proxy_async_smem();
         __syncwarp();
+        if (lane == 0) mbar_arrive(bar_xsc(kt));
+      };
+      if (kq == 0) scale_x(0);
+      // blocks (mt, kt, item of this warp's k half)
+      const int blk_mt[3] = {0, 1, 1}, blk_kt[3] = {0, 0, 1};
+      const int blk_it[3] = {6 + kh, 8 + kh, 11 + kh};
+#pragma unroll
+      for (int bi = 0; bi < 3; ++bi) {
+        if (bi == 2 && kq == 1) scale_x(1);
+        const int item = blk_it[bi];
+        const int s = (f + item) % C::NSLOT;
+        mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
+        if (r == 0 && (kq & 1) == 0 && lu < 20) SSD_TRACE(1000 + lu * 12 + bi * 4 + kh * 2);
+        const int m = blk_mt[bi] * 128 + r;  // row within the chunk
+        const float am = va[m];
+        const uint32_t row = sRing + s * SLOT + r * 128;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {  // the thread's two K steps (16 keys each)
+          const int k0 = blk_kt[bi] * 128 + 32 * kq + 16 * ks;
+          // W[m][k] = cb[m][k] exp2(a_m - a_{k0}) for k <= m, k < len (x carries xs_k)
+          const float sc = (k0 <= m && k0 < len) ? ex2(am - va[k0]) : 0.f;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            // keys [kb, kb + 8): logical 16-B unit q of the row, stored at unit q ^ (r & 7)
+            const int q = 4 * (kq & 1) + 2 * ks + hh;
+            const int kb = k0 + 8 * hh;
+            const uint32_t addr = row + ((q ^ (r & 7)) << 4);
+            uint32_t v[4] = {0u, 0u, 0u, 0u};
+            if (kb <= m && kb < len) {  // else the whole unit is masked
+              ld_shared_v4(addr, v);
+              const bool edge = kb + 7 > m || kb + 7 >= len;  // the diagonal / last unit
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 cbv = unpack2<BF16>(v[e]);
+                float w0 = cbv.x * sc, w1 = cbv.y * sc;
+                if (edge) {
+                  const int k = kb + 2 * e;
+                  if (k > m || k >= len) w0 = 0.f;
+                  if (k + 1 > m || k + 1 >= len) w1 = 0.f;
+                }
+                v[e] = pack2rn<BF16>(w0, w1);
+              }
+            }
+            st_shared_v4(addr, v[0], v[1], v[2], v[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (r == 0 && (kq & 1) == 0 && lu < 20) SSD_TRACE(1000 + lu * 12 + bi * 4 + kh * 2 + 1);
         if (lane == 0) mbar_arrive(bar_built(2 * bi + kh));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_vec_empty(vb));
     }
-  } else if (warp >= 12) {
+  } else if (warp >= C::EPI_WARP0) {
     // ===== epilogue: out[m][p] = exp(dA[m]) O1 + O2 + D x  (TMEM lane m of each row tile) =====
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
@@ -535,14 +643,15 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       const int vb = lu & 1;
       const float Dh = p.D ? p.D[h] : 0.f;
       mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
-      const float* vdA = vec + vb * 2 * Q;
+      const float* va = vec + vb * 2 * Q;
       mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
+      if (r == 0 && lu < 20) SSD_TRACE(1600 + lu * 2);
       tc_fence_after();
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int m = mt * 128 + r;
         const int t = c * Q + m;
-        const float sm = exp2f(vdA[m] * LOG2E);
+        const float sm = ex2(va[m]);
         const uint32_t tacc = tmem_base + lane_off + a * 256 + 128 * mt;
         const size_t ro = (((size_t)b * p.L + t) * p.H + h) * P;  // element offset of row t
         const bool ok = t < p.L;
@@ -558,8 +667,8 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
             uint32_t pk[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint4 xv = __ldg(xs + q);
-              const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+              const uint4 xq = __ldg(xs + q);
+              const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 xf = unpack2<BF16>(xw[e]);
@@ -578,6 +687,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       }
       tc_fence_before();
       __syncwarp();
+      if (r == 0 && lu < 20) SSD_TRACE(1600 + lu * 2 + 1);
       if (lane == 0) {
         mbar_arrive(bar_acc_empty(a));
         mbar_arrive(bar_vec_empty(vb));

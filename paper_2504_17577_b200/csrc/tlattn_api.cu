@@ -995,6 +995,7 @@ extern "C" int tl_ssd_chunk_state(const void* x, const void* Bm, const float* dt
   prm.nc = (seqlen + chunk_size - 1) / chunk_size;
   prm.grp = nheads / ngroups;
   prm.n_units = batch * prm.nc * (nheads / 2);
+  prm.trace = g_trace;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   rc = dtype == TL_DTYPE_BF16
            ? ssd_launch(ssd::tl_ssd_state_kernel<true>, ssd::StateCfg::SMEM_BYTES, ssd::StateCfg::THREADS, prm, *di, 18, st)
@@ -1046,6 +1047,7 @@ extern "C" int tl_ssd_chunk_scan(const void* cb, const void* x, const float* dt,
   prm.nc = nc;
   prm.grp = nheads / ngroups;
   prm.n_units = batch * nc * nheads;
+  prm.trace = g_trace;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   rc = dtype == TL_DTYPE_BF16
            ? ssd_launch(ssd::tl_ssd_scan_kernel<true>, ssd::ScanCfg::SMEM_BYTES, ssd::ScanCfg::THREADS, prm, *di, 20, st)
