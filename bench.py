@@ -397,6 +397,9 @@ def run_ours(args, world, rank, local):
         from paper_2504_17577_b200.configs import MLA_CONFIGS
         for mc in MLA_CONFIGS:  # MLA decode (Fig. 18)
             extra["mla_" + mc.name] = bench_mla(mc, pk, steps=max(5, min(args.steps, 20)))
+        from paper_2504_17577_b200.configs import SSD_CONFIGS
+        for sname in ("CT5", "CC5", "CT3", "CC3"):  # Mamba-2 SSD (Table 4)
+            extra["ssd_" + sname] = bench_ssd(SSD_CONFIGS[sname], pk, steps=max(5, min(args.steps, 10)))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -506,6 +509,48 @@ def bench_mla(cfg, pk, steps=20, warmup=3):
            "frac_of_peak": tf / pk["burst"], "launches_per_call": tl_attn_last_launch_count(),
            "bound": "hbm", **cfg.as_dict()}
     del q, qp, kv, kp, o, lse, ws
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_ssd(cfg, pk, steps=10, warmup=3):
+    """Mamba-2 SSD chunk_state (CT) / chunk_scan (CC) on a Table 4 shape (PAPER.md
+    P:L464-478). Bound: HBM (80-97 FLOP/B); GB/s of the algorithmic bytes (every input read
+    once, the output written once; configs.SsdConfig.hbm_bytes)."""
+    from paper_2504_17577_b200 import ssd_chunk_scan, ssd_chunk_state, tl_attn_last_launch_count
+    from paper_2504_17577_b200.inputs import gen_ssd, gen_ssd_cb_prev, ssd_chunked_dt
+    x, Bm, C, dtv, A, D = gen_ssd(cfg.B, cfg.L, cfg.H, cfg.G, cfg.P, cfg.N, cfg.dtype, cfg.seed,
+                                  "cuda")
+    dt, dA = ssd_chunked_dt(dtv, A, cfg.Q)
+    if cfg.kind == "state":
+        out = torch.empty((cfg.B, cfg.nc, cfg.H, cfg.P, cfg.N), dtype=cfg.dtype, device="cuda")
+
+        def call():
+            ssd_chunk_state(x, Bm, dt, dA, out=out)
+    else:
+        cb, prev = gen_ssd_cb_prev(cfg.B, cfg.L, cfg.H, cfg.G, cfg.P, cfg.N, cfg.dtype, cfg.seed,
+                                   "cuda")
+        out = torch.empty_like(x)
+
+        def call():
+            ssd_chunk_scan(cb, x, dt, dA, C, prev, D, out=out)
+    for _ in range(warmup):
+        call()
+    st = torch.cuda.current_stream()
+    evs = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        call()
+        b.record(st)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    gbs = cfg.hbm_bytes() / (ms * 1e-3) / 1e9
+    res = {"us": ms * 1e3, "hbm_gbs": gbs, "frac_of_hbm": gbs / pk["hbm"],
+           "tflops": cfg.flops() / (ms * 1e-3) / 1e12, "bound": "hbm",
+           "launches_per_call": tl_attn_last_launch_count(), **cfg.as_dict()}
+    del x, Bm, C, out
     torch.cuda.empty_cache()
     return res
 

@@ -12,6 +12,9 @@ LIB = os.path.join(PKG, "libtlattn.so")
 SOURCES = [os.path.join(CSRC, "tlattn_api.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "tlattn.h")]
+# the seeded input generator as one CUDA kernel (test / bench infrastructure, inputs.py)
+GEN_LIB = os.path.join(PKG, "libtlgen.so")
+GEN_SRC = os.path.join(CSRC, "gen.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -23,10 +26,11 @@ NVCC_FLAGS = [
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(GEN_LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS if os.path.exists(p))
+    return any(os.path.getmtime(p) > t for p in DEPS if os.path.exists(p)) or \
+        os.path.getmtime(GEN_SRC) > os.path.getmtime(GEN_LIB)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -41,6 +45,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(tmp, LIB)
+    tmpg = GEN_LIB + f".tmp{os.getpid()}"
+    r = subprocess.run([NVCC, *NVCC_FLAGS, "-o", tmpg, GEN_SRC], capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libtlgen.so")
+    os.replace(tmpg, GEN_LIB)
     return LIB
 
 

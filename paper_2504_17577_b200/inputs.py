@@ -11,7 +11,9 @@ slice) is bit-identical to the same slice of the unsharded tensor.
 
 Generator: u32 = lowbias32(counter ^ key) (two rounds), uniforms from the top 24 bits,
 Box-Muller in fp32. Integer hashing is done in int64 torch ops masked to 32 bits so
-it runs identically on CPU and CUDA tensors.
+it runs identically on CPU and CUDA tensors. On CUDA devices gen_tensor runs the same
+generator as ONE kernel per tensor (csrc/gen.cu, libtlgen.so; bit-identical to the torch
+ops, tests/test_inputs_gpu.py) instead of dozens of elementwise launches per chunk.
 """
 from __future__ import annotations
 
@@ -64,8 +66,48 @@ def uniform_from_index(idx: torch.Tensor, seed: int, tensor_id: int) -> torch.Te
     return ((h >> 8).to(torch.float32) + 0.5) * (1.0 / 16777216.0)
 
 
+_gen_lib = None
+
+
+def _gen_library():
+    """libtlgen.so (built by build.py next to libtlattn.so), or None if absent."""
+    global _gen_lib
+    if _gen_lib is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtlgen.so")
+        if not os.path.exists(path):
+            return None
+        lib = ctypes.CDLL(path)
+        P, I = ctypes.c_void_p, ctypes.c_int
+        lib.tl_gen_normal.argtypes = [P, I, I, P, P, P, ctypes.c_uint32, P]
+        lib.tl_gen_normal.restype = I
+        _gen_lib = lib
+    return _gen_lib
+
+
+def _gen_cuda(out, shape, ranges, tid, seed, use_kernel=True):
+    import numpy as np_
+    lib = _gen_library() if use_kernel else None
+    if lib is None:
+        return False
+    code = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}.get(out.dtype)
+    if code is None:
+        return False
+    nd = len(shape)
+    sh = np_.array(shape, np_.int64)
+    st = np_.array([r.start for r in ranges], np_.int64)
+    osz = np_.array([len(r) for r in ranges], np_.int64)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    rc = lib.tl_gen_normal(out.data_ptr(), code, nd, sh.ctypes.data, st.ctypes.data,
+                           osz.ctypes.data, _key(seed, tid), stream)
+    if rc != 0:
+        raise RuntimeError(f"tl_gen_normal failed ({rc})")
+    return True
+
+
 def gen_tensor(shape, seed: int, name: str, dtype: torch.dtype, device,
-               slices=None, chunk: int = 1 << 25) -> torch.Tensor:
+               slices=None, chunk: int = 1 << 25, use_kernel: bool = True) -> torch.Tensor:
     """Contiguous tensor of ``shape`` (global BSHD shape), optionally a sub-block.
 
     ``slices`` is a tuple of python ``slice`` objects over the global shape (step 1);
@@ -89,6 +131,8 @@ def gen_tensor(shape, seed: int, name: str, dtype: torch.dtype, device,
     for i in range(len(out_shape) - 2, -1, -1):
         out_strides[i] = out_strides[i + 1] * out_shape[i + 1]
     tid = TENSOR_ID[name]
+    if out.is_cuda and len(shape) <= 6 and _gen_cuda(out, shape, ranges, tid, seed, use_kernel):
+        return out
     for start in range(0, n, chunk):
         stop = min(n, start + chunk)
         loc = torch.arange(start, stop, dtype=torch.int64, device=device)

@@ -199,3 +199,29 @@ def test_options_set_get_without_a_device(lib):
     assert lib.tl_attn_get_option(TL_OPT_LPT) == old
     assert lib.tl_attn_set_option(TL_OPT_LPT, -7) == 0 and lib.tl_attn_get_option(TL_OPT_LPT) == -1
     lib.tl_attn_set_option(TL_OPT_LPT, old)
+
+
+def test_ssd_argument_errors_before_any_cuda_call(lib):
+    """tl_ssd_chunk_state / _scan validate their arguments before touching the device."""
+    F = FAKE
+    st = lambda **o: lib.tl_ssd_chunk_state(  # noqa: E731
+        o.get("x", F), o.get("b", F), o.get("dt", F), o.get("dA", F), o.get("out", F),
+        o.get("B", 1), o.get("L", 256), o.get("H", 2), o.get("G", 1), o.get("P", 64),
+        o.get("N", 128), o.get("Q", 256), o.get("dtype", 1), None)
+    sc = lambda **o: lib.tl_ssd_chunk_scan(  # noqa: E731
+        o.get("cb", F), o.get("x", F), o.get("dt", F), o.get("dA", F), o.get("c", F),
+        o.get("prev", F), o.get("D", None), o.get("out", F), o.get("B", 1), o.get("L", 256),
+        o.get("H", 2), o.get("G", 1), o.get("P", 64), o.get("N", 128), o.get("Q", 256),
+        o.get("dtype", 1), None)
+    for call in (st, sc):
+        assert call(x=None) == 1
+        assert call(B=0) == 1
+        assert call(H=3, G=2) == 1          # nheads % ngroups
+        assert call(dtype=7) == 1
+        assert call(P=32) == 2              # head_dim 64 only
+        assert call(N=64) == 2              # d_state 128 only
+        assert call(Q=128) == 2             # chunk length 256 only
+        assert call(x=F + 8) == 2           # 16-byte alignment
+    assert st(H=3, G=1) == 2                # chunk_state: head pairs
+    assert st(H=4, G=4) == 2                # both heads of a pair in one group
+    assert sc(dt=F + 2) == 2                # fp32 vectors: 4-byte alignment
