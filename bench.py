@@ -376,9 +376,13 @@ def run_ours(args, world, rank, local):
         e_ms = e_total / args.e2e_steps
         h2d = sum(t.numel() * t.element_size() for t in (qh, kh, vh))
         d2h = oh.numel() * oh.element_size() + lh.numel() * 4
+        # transfer floor of the same bytes: pinned-memory copies alone (one H2D of q's size
+        # and one D2H of o's size, timed like the step), scaled to the step's byte counts
+        floor = pcie_floor(qh, oh, h2d, d2h)
         e2e = {"value": flop / (e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "steps": args.e2e_steps, "api": "tl_attn_fwd_host (pinned host buffers)"}
+               "steps": args.e2e_steps, "api": "tl_attn_fwd_host (pinned host buffers)",
+               **floor, "frac_of_transfer_floor": floor["transfer_floor_ms"] / e_ms}
         del qh, kh, vh, oh, lh, ha
 
     extra = {}
@@ -424,6 +428,28 @@ def run_ours(args, world, rank, local):
                 "gather_ms": gather_ms,
                 "also": extra}
         print(json.dumps(line), flush=True)
+
+
+def pcie_floor(src_h, dst_h, h2d_bytes, d2h_bytes):
+    """Measured pinned host<->device copy bandwidth (one copy each way, CUDA events) and the
+    resulting floor for a step that moves h2d_bytes up and d2h_bytes down with the two
+    directions overlapped (the host entry pipelines them): max(h2d/bw_up, d2h/bw_down)."""
+    dev = torch.empty(src_h.shape, dtype=src_h.dtype, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    dev.copy_(src_h, non_blocking=True)
+    torch.cuda.synchronize()
+    ev[0].record()
+    dev.copy_(src_h, non_blocking=True)
+    ev[1].record()
+    ev[2].record()
+    dst_h.copy_(dev, non_blocking=True)
+    ev[3].record()
+    torch.cuda.synchronize()
+    up = src_h.numel() * src_h.element_size() / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+    down = dst_h.numel() * dst_h.element_size() / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
+    del dev
+    return {"h2d_gbs_measured": up, "d2h_gbs_measured": down,
+            "transfer_floor_ms": max(h2d_bytes / up, d2h_bytes / down) / 1e6}
 
 
 def ncu_traffic(name, world):

@@ -320,12 +320,29 @@ __device__ __forceinline__ void exp_row(float* s, float c, float m_use, uint32_t
 
 // Mask columns [C0, C0+NC) of a diagonal / tail block (k0 + col > limit -> -inf) and
 // return their max (T.reduce_max: in-thread, each thread owns one whole S row).
+// The 32 rows of a warp are consecutive, so their limits span at most 32 keys: a 32-column
+// chunk that every lane sees whole is skipped with one warp-uniform test, and the compare
+// of the other chunks is against a per-chunk bound (ISETP with an immediate + SEL per
+// element). The naive form (VIADD + ISETP + SEL on all 128 columns, ALU pipe at half rate)
+// measured ~900 extra SM clocks per diagonal block on C5 (profiles/r02_kernel_notes.md).
+// Variants that also skipped fully masked chunks in the exp pass measured slower on every
+// config (larger code on the unmasked path, or register spills: r02 notes).
 template <int C0, int NC>
 __device__ __forceinline__ float mask_max_cols(float* s, int k0, int limit, bool masked) {
+#ifdef TLATTN_NO_MASK  // timing experiment only (WRONG results): no causal / tail mask
+  masked = false;
+#endif
   if (masked) {
+    const int lim_lo = __shfl_sync(0xffffffffu, limit, 0);  // rows ascend with the lane
 #pragma unroll
-    for (int cc = C0; cc < C0 + NC; ++cc)
-      if (k0 + cc > limit) s[cc] = -INFINITY;
+    for (int q = 0; q < NC / 32; ++q) {
+      const int c0 = k0 + C0 + 32 * q;
+      if (c0 + 31 > lim_lo) {       // not every lane sees the whole chunk
+        const int nv = limit - c0;  // this lane sees columns e <= nv of the chunk
+#pragma unroll
+        for (int e = 0; e < 32; ++e) s[C0 + 32 * q + e] = e > nv ? -INFINITY : s[C0 + 32 * q + e];
+      }
+    }
   }
   constexpr int R = NC / 32;
   float mq[R];

@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(256, 1) kern(float* out, int iters, long long*
     for (int i = 0; i < NC; ++i) sl[i] = s[i] + 1e-7f * it;  // fresh "S" every block
     float mx = 0.f;
     if (MODE == 3) mx = mask_max_cols<0, NC>(sl, 0, (threadIdx.x & 127) * NC / 128, true);  // diagonal block
+    else if (MODE == 4) mx = mask_max_cols<0, NC>(sl, 0, -1, true);  // fully masked rows
+    else if (MODE == 5) mx = mask_max_cols<0, NC>(sl, 0, (threadIdx.x & 127) * NC / 128 - 64, true);
     else if (MODE != 2) mx = mask_max_cols<0, NC>(sl, 0, 1 << 30, false);
     float m_new, alpha, m_use;
     row_max_finish(mx, 1.4426950408889634f * 0.0883883f, m, m_new, alpha, m_use);
@@ -64,6 +66,8 @@ void run(const char* name, int warps) {
 int main() {
   run<64, 0, 0>("64col emu0", 8);
   run<128, 0, 3>("128col emu0 masked (2 tiles)", 8);
+  run<128, 0, 4>("128col emu0 all -inf (2 tiles)", 8);
+  run<128, 0, 5>("128col emu0 masked-64 (2 tiles)", 8);
   run<128, 0, 0>("128col emu0 unmasked (2 tiles)", 8);
   run<64, 1, 0>("64col emu1", 8);
   run<64, 2, 0>("64col emu2", 8);
