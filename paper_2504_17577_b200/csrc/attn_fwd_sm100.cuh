@@ -15,6 +15,16 @@
 //                 exp2, row sum, O rescale in TMEM, P -> smem
 //                 (128B-swizzled, RN to dtype), epilogue O/l and LSE
 //
+// Row reductions (max, sum) are IN-THREAD, not warp shuffles: tcgen05.ld 32x32b gives each
+// thread one whole TMEM lane = one S row, so there is nothing to shuffle. The shuffle-free
+// alternative on this layout — two or four threads per row with a cross-warp exchange
+// through SMEM — was measured at D = 128 on B200 (round 2, profiles/r02_kernel_notes.md):
+// in isolation its exp/max/sum work is ~10 % cheaper (two warps per SM sub-partition feed
+// MUFU), but in the kernel every schedule built around it was slower (T0 1233 / 1042 / 1010
+// TFLOP/s vs 1421-1430 one-thread-per-row: lock-step warps expose the TMEM-load, barrier
+// and proxy-fence latencies, and 16 softmax warps leave 96 registers per thread); at D = 64
+// a 640-thread split-row variant measured C4 657 vs 664 (round 1).
+//
 // TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D)
 // SMEM: Q0,Q1 (2 x 128 x D x 2B) | KV ring NST x (128 x D x 2B) | P0,P1 (2 x 32 KB) | mbarriers
 // All operand tiles are TMA SWIZZLE_128B boxes of 128 rows x 64 elements (16 KB).
