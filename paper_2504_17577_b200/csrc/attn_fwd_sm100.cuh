@@ -133,7 +133,16 @@ __device__ __forceinline__ int n_outputs(const PT& p) {
     if (p.trace != nullptr && blockIdx.x < 2 && (k) < 4)                                 \
       p.trace[(idx) + 200 * (k) + 8000 * blockIdx.x] = clock64();                        \
   } while (0)
+// per-CTA globaltimer spans (all CTAs): slot 0 kernel entry, 1 + 3k / 2 + 3k first S /
+// O store issued of unit k < 4 (tile 0), 15 kernel end
+#define TL_SPAN(idx)                                                                     \
+  do {                                                                                   \
+    if (p.trace != nullptr) p.trace[16000 + 16 * blockIdx.x + (idx)] = globaltimer();    \
+  } while (0)
 #else
+#define TL_SPAN(idx) \
+  do {               \
+  } while (0)
 #define TL_TRACE2(k, idx) \
   do {                    \
   } while (0)
@@ -600,8 +609,10 @@ tl_attn_fwd_kernel(const __grid_constant__ PT p) {
     // S buffer frees early), then PV_t(j) once P_t(j) is written. The tensor pipe
     // interleaves the two streams. K/V slots, the Q buffer and the scheduler slot are
     // released by BOTH issuers (barrier counts 2).
+    // Whole warp: uniform control flow, tcgen05 ops by one elected lane (elect_one(): the
+    // descriptors stay in uniform registers, no per-MMA R2UR loop).
     const int t = warp - 1;
-    if (lane == 0) {
+    {
       constexpr uint32_t FMT = BF16 ? 1u : 0u;
       // S = Q K^T: A = Q (K-major), B = K (K-major), M=128, N=128; a_negate if scale < 0
       const uint32_t IDESC_QK = make_idesc_f16(FMT, BM, BN, 0, 0, p.neg ? 1u : 0u);
@@ -648,11 +659,12 @@ tl_attn_fwd_kernel(const __grid_constant__ PT p) {
             // K-major SW128: a 16-element K step is +32 B inside the 128-B swizzle row;
             // every 64 elements the next 16 KB TMA box
             const uint32_t off = (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32;
-            mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
-                       make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
+            if (elect_one())
+              mma_f16_ss(tm_s, make_sdesc_sw128(qa + off, 16, 1024),
+                         make_sdesc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0 ? 1u : 0u);
           }
-          mma_commit(bar_s_full(t));
-          mma_commit(bar_kv_empty(kslot(j)));  // this tile is done with K_j
+          if (elect_one()) mma_commit(bar_s_full(t));
+          if (elect_one()) mma_commit(bar_kv_empty(kslot(j)));  // this tile is done with K_j
           ++cs;
         };
         // O_t += P_t V_j
@@ -673,41 +685,44 @@ tl_attn_fwd_kernel(const __grid_constant__ PT p) {
             const uint64_t bd = make_sdesc_sw128(vb + kk * 2048, CHUNK_BYTES, 1024);
             if constexpr (C::P_TMEM) {
               // A = P_t in TMEM: 16 keys = 8 columns of packed 16-bit pairs
-              mma_f16_ts(tm_o, tm_p + kk * 8, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+              if (elect_one())
+                mma_f16_ts(tm_o, tm_p + kk * 8, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
             } else {
               // A = P (K-major SW128, 2 x 16 KB key chunks)
               const uint64_t ad = make_sdesc_sw128(pa + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
-              mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+              if (elect_one())
+                mma_f16_ss(tm_o, ad, bd, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
             }
           }
-          mma_commit(bar_o_done(t));
-          mma_commit(bar_kv_empty(vslot(j)));  // this tile is done with V_j
+          if (elect_one()) mma_commit(bar_o_done(t));
+          if (elect_one()) mma_commit(bar_kv_empty(vslot(j)));  // this tile is done with V_j
           ++cpv;
         };
         if (nt > 0) {
           issue_s(0);
-          if (nt == 1) mma_commit(bar_q_empty);
+          if ((nt == 1) && elect_one()) mma_commit(bar_q_empty);
           for (int j = 0; j < nt; ++j) {
             if (j + 1 < nt) {
               issue_s(j + 1);
-              if (j + 2 == nt) mma_commit(bar_q_empty);  // last QK^T of this tile issued
+              // last QK^T of this tile issued
+              if ((j + 2 == nt) && elect_one()) mma_commit(bar_q_empty);
             }
             issue_pv(j);
           }
         } else {
-          mbar_arrive(bar_q_empty);
+          if (elect_one()) mbar_arrive(bar_q_empty);
         }
         // blocks this tile skips (causal): release its share of their K/V slots, after the
         // slot holds that block (so the arrival counts toward the right phase)
         for (int j = nt; j < nmax; ++j) {
           mbar_wait(bar_kv_full(kslot(j)), kpar(j));
-          mbar_arrive(bar_kv_empty(kslot(j)));
+          if (elect_one()) mbar_arrive(bar_kv_empty(kslot(j)));
           mbar_wait(bar_kv_full(vslot(j)), vpar(j));
-          mbar_arrive(bar_kv_empty(vslot(j)));
+          if (elect_one()) mbar_arrive(bar_kv_empty(vslot(j)));
         }
         mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
         const int nxt = clc_query(sSched + 16 * (k & 1));
-        mbar_arrive(bar_sched_empty(k & 1));
+        if (elect_one()) mbar_arrive(bar_sched_empty(k & 1));
         if (nxt < 0) break;
         unit = nxt;
       }

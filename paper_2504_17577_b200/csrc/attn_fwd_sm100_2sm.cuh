@@ -122,6 +122,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
+    TL_SPAN(0);
     prefetch_tmap(&p.tm_q);
     prefetch_tmap(&p.tm_k);
     prefetch_tmap(&p.tm_v);
@@ -364,6 +365,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
       for (int j = 0; j < nt; ++j, ++g) {
         mbar_wait(bar_s_full(t), g & 1);
         if (lane == 0 && q4 == 0) TL_TRACE2(k, 1000 * t + 8 * j + 0);
+        if (j == 0 && k < 4 && t == 0 && lane == 0 && q4 == 0) TL_SPAN(1 + 3 * k);
         tc_fence_after();
         uint32_t sr[BN];
 #pragma unroll
@@ -532,6 +534,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           }
         }
         tma_store_commit();
+        if (k < 4 && t == 0) TL_SPAN(2 + 3 * k);
       }
       if (row_ok)
         store_lse(p, U.b, U.h, row, (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY);
@@ -547,6 +550,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
 
   if (warp >= SOFTMAX_WARP0 && ((warp - SOFTMAX_WARP0) & 3) == 0 && lane == 0)
     tma_store_wait_all<0>();  // O stores complete before the CTA's smem goes away
+  if (warp == SOFTMAX_WARP0 && lane == 0) TL_SPAN(15);
   tc_fence_before();
   cluster_sync();  // both CTAs finished with TMEM / smem of the pair
   if (warp == 1) {

@@ -20,7 +20,7 @@
 //     B = Bm [N = 128 n][K] (MN-major), D = states in TMEM (double-buffered over units), the
 //     epilogue warps convert and store each (h, p) row (256 B). Consecutive units share (b, c),
 //     so the Bm tile of a chunk is read from HBM once and from L2 by the other head pairs.
-//   * chunk_scan unit = (b, c, h), two M = 128 row tiles: O1 = C [m][n] . prev [p][n]^T
+//   * chunk_scan unit = (b, c, h, row tile of 128): O1 = C [m][n] . prev [p][n]^T
 //     (both K-major, K = n = 128), O2 = W [m][k] . x [k][p] (x MN-major, K = k) with
 //     the decay split per MMA K step of 16 keys: exp(dA_m - dA_k) dt_k =
 //     exp2(a_m - a_{k0(k)}) * [dt_k exp2(a_{k0(k)} - a_k)] with a = dA log2 e; the second
@@ -317,24 +317,33 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
 }
 
 // ============================================================================ chunk_scan
-// Per-unit ring items (16 KB slots), in the order the MMA consumes them:
-//   0 S (prev [64 p][128 n], 2 boxes) | 1-2 C rows 0-127 (n halves) | 3-4 C rows 128-255 |
-//   5 x rows 0-127 | 6-7 cb (m 0-127, k 0-127: k halves) | 8-9 cb (m 128-255, k 0-127) |
-//   10 x rows 128-255 | 11-12 cb (m 128-255, k 128-255)
-// Both C . prev GEMMs run first, so the slots free up in about the order they were filled
-// and the next unit's S and C stream in while this unit's W blocks are still being used.
+// Unit = (b, c, h, row tile mt) — one 128-row tile per unit, so about two units fit in the
+// slot ring and one unit's W build overlaps the next unit's loads (a unit holding both row
+// tiles needed 13 of the 12 slots and serialised load -> W build -> GEMM per unit). Ring
+// items (16 KB slots) in MMA consumption order:
+//   mt = 0: 0 S (prev [64 p][128 n], 2 boxes) | 1-2 C rows 0-127 (n halves) | 3 x rows 0-127 |
+//           4-5 cb (m 0-127, k 0-127: k halves)
+//   mt = 1: 0 S | 1-2 C rows 128-255 | 3 x rows 0-127 | 4-5 cb (m 128-255, k 0-127) |
+//           6 x rows 128-255 | 7-8 cb (m 128-255, k 128-255)
+// S and x rows 0-127 are read by both row-tile units of a (b, c, h) (adjacent units, on
+// neighbouring CTAs at the same time: L2 hits). The grid is odd, so every persistent CTA
+// alternates the lighter mt = 0 and the heavier mt = 1 units.
 struct ScanCfg {
   static constexpr int NSLOT = 12;
-  static constexpr int ITEMS = 13;
+  static constexpr int NACC = 4;  // TMEM accumulator buffers (O1 | O2: 128 columns each)
   static constexpr int OFF_RING = 0;
-  static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // dA, log2 dt of the unit: 2 x Q f32
+  static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // a, xs of the unit: 2 x Q f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * Q * 4;   // double-buffered over units
-  // full[NSLOT] empty[NSLOT] built[6] acc_full[2] acc_empty[2] vec_full[2] vec_empty[2]
-  // xsc[2] (x rows k-tile 0 / 1 scaled by xs).
-  // built[2 * block + k half] completes once per unit (W blocks (m0,k0) (m1,k0) (m1,k1)):
-  // a per-slot "built" barrier would complete only on the slot's W fills and fall out of
-  // step with the fill count that the waiters' parity follows.
-  static constexpr int NUM_BARS = 2 * NSLOT + 6 + 8 + 2;
+  // full[NSLOT] empty[NSLOT] built[2][4] acc_full[NACC] acc_empty[NACC] vec_full[2]
+  // vec_empty[2] xsc[2][2]. built[set][2 * block + k half] (block 0 = the k-tile 0 W block;
+  // block 1 = the diagonal block of a mt = 1 unit) and xsc[set][kt] belong to the unit's
+  // parity set = lu & 1 and complete once per unit that uses them (units alternate mt, so a
+  // set's barriers see one phase per use: wait parity (lu >> 1) & 1). Two sets let the W
+  // warps run one unit ahead of the MMA; they cannot run two ahead because that unit's cb
+  // slots are only refilled after the MMA released this unit's. (A per-slot "built" barrier
+  // would complete only on that slot's W fills and fall out of step with the fill-count
+  // parity its waiters follow.)
+  static constexpr int NUM_BARS = 2 * NSLOT + 8 + 2 * NACC + 4 + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
   // warps: 0 TMA, 1 MMA, 2 unit vectors, 4-19 W builders (4 key quarters x 4 lane
@@ -342,6 +351,7 @@ struct ScanCfg {
   static constexpr int THREADS = 24 * 32;
   static constexpr int W_WARP0 = 4, EPI_WARP0 = 20;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
+  __host__ __device__ static constexpr int items(int mt) { return mt ? 9 : 6; }
 };
 
 template <bool BF16>
@@ -357,12 +367,14 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   const uint32_t bar0 = base + C::OFF_BAR;
   auto bar_full = [&](int s) { return bar0 + 8u * s; };
   auto bar_empty = [&](int s) { return bar0 + 8u * (C::NSLOT + s); };
-  auto bar_built = [&](int w) { return bar0 + 8u * (2 * C::NSLOT + w); };
-  auto bar_acc_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 6 + i); };
-  auto bar_acc_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + i); };
-  auto bar_vec_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 10 + i); };
-  auto bar_vec_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 12 + i); };
-  auto bar_xsc = [&](int kt) { return bar0 + 8u * (2 * C::NSLOT + 14 + kt); };
+  auto bar_built = [&](int set, int w) { return bar0 + 8u * (2 * C::NSLOT + 4 * set + w); };
+  auto bar_acc_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + i); };
+  auto bar_acc_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + C::NACC + i); };
+  auto bar_vec_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + 2 * C::NACC + i); };
+  auto bar_vec_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 10 + 2 * C::NACC + i); };
+  auto bar_xsc = [&](int set, int kt) {
+    return bar0 + 8u * (2 * C::NSLOT + 12 + 2 * C::NACC + 2 * set + kt);
+  };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -376,11 +388,15 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       mbar_init(bar_full(s), 1);
       mbar_init(bar_empty(s), 1);
     }
-    for (int w = 0; w < 6; ++w) mbar_init(bar_built(w), 8);  // the 8 W warps of one k half
-    for (int kt = 0; kt < 2; ++kt) mbar_init(bar_xsc(kt), 4);  // one W lane-quarter group
-    for (int i = 0; i < 2; ++i) {
+    for (int set = 0; set < 2; ++set) {
+      for (int w = 0; w < 4; ++w) mbar_init(bar_built(set, w), 8);  // 8 W warps of a k half
+      for (int kt = 0; kt < 2; ++kt) mbar_init(bar_xsc(set, kt), 4);  // one lane-quarter group
+    }
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(bar_acc_full(i), 1);
       mbar_init(bar_acc_empty(i), 4);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(bar_vec_full(i), 1);
       mbar_init(bar_vec_empty(i), 16 + 4);  // W warps + epilogue warps
     }
@@ -392,10 +408,13 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_smem;
 
-  // unit u -> (b, c, h); consecutive units share (b, c): C and cb of the chunk from L2
-  auto decode = [&](int u, int& b, int& c, int& h) {
-    h = u % p.H;
-    const int bc = u / p.H;
+  // unit u -> (b, c, h, mt); the two row tiles of a (b, c, h) are adjacent units, and
+  // consecutive (b, c, h) share (b, c): C and cb of the chunk stay in L2
+  auto decode = [&](int u, int& b, int& c, int& h, int& mt) {
+    mt = u & 1;
+    const int bch = u >> 1;
+    h = bch % p.H;
+    const int bc = bch / p.H;
     c = bc % p.nc;
     b = bc / p.nc;
   };
@@ -403,15 +422,16 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   if (warp == 0) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-      const uint64_t pol_s = policy_evict_first();   // x, prev: read once
-      const uint64_t pol_l = policy_evict_last();    // C, cb: re-read by the chunk's other heads
+      const uint64_t pol_s = policy_evict_first();   // prev: read by the 2 row-tile units
+      const uint64_t pol_l = policy_evict_last();    // C, cb, x: re-read by other units
       int f = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        int b, c, h;
-        decode(u, b, c, h);
+        int b, c, h, mt;
+        decode(u, b, c, h, mt);
         const int g = h / p.grp;
         const int bc = b * p.nc + c;
-        for (int item = 0; item < C::ITEMS; ++item, ++f) {
+        const int ni = C::items(mt);
+        for (int item = 0; item < ni; ++item, ++f) {
           const int s = f % C::NSLOT;
           if (f >= C::NSLOT) mbar_wait(bar_empty(s), ((f / C::NSLOT) - 1) & 1);
           mbar_arrive_expect_tx(bar_full(s), SLOT);
@@ -423,19 +443,14 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
               tma_load_4d(dst, &p.tm_s, fb, 0, 0, h, bc, pol_s);
               tma_load_4d(dst + 8192, &p.tm_s, fb, 64, 0, h, bc, pol_s);
               break;
-            case 1: case 2: case 3: case 4: {  // C [128 t][64 n] (row tile, n half)
-              const int mt = item >= 3, nh = (item - 1) & 1;
-              tma_load_4d(dst, &p.tm_c, fb, 64 * nh, g, c * Q + 128 * mt, b, pol_l);
+            case 1: case 2:  // C [128 t][64 n] of this row tile, n halves
+              tma_load_4d(dst, &p.tm_c, fb, 64 * (item - 1), g, c * Q + 128 * mt, b, pol_l);
               break;
-            }
-            case 5: case 10: {  // x [128 k][64 p]
-              const int kt = item == 10;
-              tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * kt, b, pol_s);
+            case 3: case 6:  // x [128 k][64 p] of k-tile 0 / 1
+              tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * (item == 6), b, pol_l);
               break;
-            }
-            default: {  // cb [128 m][64 k]: items 6,7 (m0 k0), 8,9 (m1 k0), 11,12 (m1 k1)
-              const int mt = item >= 8, kt = item >= 11;
-              const int kh = (item == 7 || item == 9 || item == 12);
+            default: {  // cb [128 m][64 k]: items 4,5 (k-tile 0), 7,8 (k-tile 1)
+              const int kt = item >= 7, kh = (item == 5 || item == 8);
               tma_load_4d(dst, &p.tm_cb, fb, 128 * kt + 64 * kh, 128 * mt, g, bc, pol_l);
               break;
             }
@@ -449,66 +464,63 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     constexpr uint32_t FMT = BF16 ? 1u : 0u;
     constexpr uint32_t IDESC1 = make_idesc_f16(FMT, 128, P, 0, 0, 0);  // C . prev^T (K-major)
     constexpr uint32_t IDESC2 = make_idesc_f16(FMT, 128, P, 0, 1, 0);  // W . x (x MN-major)
-    int f = 0, lu = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu, f += C::ITEMS) {
-      const int a = lu & 1;
-      if (lu >= 2) mbar_wait(bar_acc_empty(a), ((lu >> 1) - 1) & 1);
+    int f = 0, lu = 0;  // ring fills and units so far
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      int b, c, h, mt;
+      decode(u, b, c, h, mt);
+      const int a = lu % C::NACC;
+      if (lu >= C::NACC) mbar_wait(bar_acc_empty(a), ((lu / C::NACC) - 1) & 1);
       tc_fence_after();
       auto slot = [&](int item) { return (f + item) % C::NSLOT; };
       auto par = [&](int item) { return ((f + item) / C::NSLOT) & 1; };
       auto saddr = [&](int item) { return sRing + slot(item) * SLOT; };
-      const uint32_t acc = tmem_base + a * 256;  // [O1 m0 | O2 m0 | O1 m1 | O2 m1] x 64 cols
-      // O1[mt] = C[mt rows] . prev^T: A items (ca, cb_) = n halves, B = item 0
-      auto gemm1 = [&](int mt, int ia, int ib) {
-        mbar_wait(bar_full(slot(0)), par(0));
-        mbar_wait(bar_full(slot(ia)), par(ia));
-        mbar_wait(bar_full(slot(ib)), par(ib));
-        tc_fence_after();
+      const uint32_t acc = tmem_base + a * 128;  // [O1 | O2] x 64 columns
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 0);
+      // O1 = C[tile rows] . prev^T: A items 1, 2 = n halves, B = item 0
+      mbar_wait(bar_full(slot(0)), par(0));
+      mbar_wait(bar_full(slot(1)), par(1));
+      mbar_wait(bar_full(slot(2)), par(2));
+      tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < N / 16; ++kk) {
-          const uint32_t asrc = saddr(kk < 4 ? ia : ib) + (kk & 3) * 32;
-          const uint32_t bsrc = saddr(0) + (kk >> 2) * 8192 + (kk & 3) * 32;
-          if (elect_one())
-            mma_f16_ss(acc + 128 * mt, make_sdesc_sw128(asrc, 16, 1024),
-                       make_sdesc_sw128(bsrc, 16, 1024), IDESC1, kk > 0 ? 1u : 0u);
-        }
+      for (int kk = 0; kk < N / 16; ++kk) {
+        const uint32_t asrc = saddr(kk < 4 ? 1 : 2) + (kk & 3) * 32;
+        const uint32_t bsrc = saddr(0) + (kk >> 2) * 8192 + (kk & 3) * 32;
+        if (elect_one())
+          mma_f16_ss(acc, make_sdesc_sw128(asrc, 16, 1024), make_sdesc_sw128(bsrc, 16, 1024),
+                     IDESC1, kk > 0 ? 1u : 0u);
+      }
+      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 1);
+      auto release = [&](int item) {
+        if (elect_one()) mma_commit(bar_empty(slot(item)));
       };
-      // O2[mt] += W[mt][kt] . x[kt]: A items (wa, wb) = k halves of W block wblk (built),
-      // B = x item
-      auto gemm2 = [&](int mt, int wblk, int wa, int wb, int xi, bool first) {
-        mbar_wait(bar_xsc(xi == 10), lu & 1);  // x~ = xs * x rows of this k-tile
-        mbar_wait(bar_built(2 * wblk), lu & 1);
-        mbar_wait(bar_built(2 * wblk + 1), lu & 1);
+      release(0), release(1), release(2);
+      // O2 += W[kt] . x~[kt] (W block wblk built, x~ scaled)
+      const int set = lu & 1;
+      const uint32_t upar = (lu >> 1) & 1;
+      auto gemm2 = [&](int wblk, int wa, int wb, int xi, int kt, bool first) {
+        mbar_wait(bar_xsc(set, kt), upar);
+        mbar_wait(bar_built(set, 2 * wblk), upar);
+        mbar_wait(bar_built(set, 2 * wblk + 1), upar);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t asrc = saddr(kk < 4 ? wa : wb) + (kk & 3) * 32;
           const uint32_t bsrc = saddr(xi) + kk * 2048;
           if (elect_one())
-            mma_f16_ss(acc + 128 * mt + 64, make_sdesc_sw128(asrc, 16, 1024),
+            mma_f16_ss(acc + 64, make_sdesc_sw128(asrc, 16, 1024),
                        make_sdesc_sw128(bsrc, 16, 1024), IDESC2, (!first || kk > 0) ? 1u : 0u);
         }
       };
-      auto release = [&](int item) {
-        if (elect_one()) mma_commit(bar_empty(slot(item)));
-      };
-      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 0);  // unit start (acc free)
-      gemm1(0, 1, 2);
-      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 1);
-      release(1), release(2);
-      gemm1(1, 3, 4);
+      gemm2(0, 4, 5, 3, 0, true);
+      release(3), release(4), release(5);
       if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 2);
-      release(0), release(3), release(4);
-      gemm2(0, 0, 6, 7, 5, true);
+      if (mt) {
+        gemm2(1, 7, 8, 6, 1, false);
+        release(6), release(7), release(8);
+      }
       if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 3);
-      release(6), release(7);
-      gemm2(1, 1, 8, 9, 5, true);
-      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 4);
-      release(5), release(8), release(9);
-      gemm2(1, 2, 11, 12, 10, false);
-      if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 5);
-      release(10), release(11), release(12);
       if (elect_one()) mma_commit(bar_acc_full(a));
+      f += C::items(mt);
     }
     __syncwarp();
   } else if (warp == 2) {
@@ -520,43 +532,43 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     // at most 16 positions of decay, <= 2^37 at the Mamba-2 initialisation ranges) ======
     int lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
-      int b, c, h;
-      decode(u, b, c, h);
+      int b, c, h, mt;
+      decode(u, b, c, h, mt);
       const int vb = lu & 1;
       if (lu >= 2) mbar_wait(bar_vec_empty(vb), ((lu >> 1) - 1) & 1);
       const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
       float* dst = vec + vb * 2 * Q;
       for (int i = lane; i < Q; i += 32) {
-        const float a = __ldg(p.dA + vo + i) * LOG2E;
+        const float av = __ldg(p.dA + vo + i) * LOG2E;
         const float a0 = __ldg(p.dA + vo + (i & ~15)) * LOG2E;
-        dst[i] = a;
-        dst[Q + i] = __ldg(p.dt + vo + i) * ex2(a0 - a);
+        dst[i] = av;
+        dst[Q + i] = __ldg(p.dt + vo + i) * ex2(a0 - av);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_vec_full(vb));  // release: smem writes visible to waiters
     }
   } else if (warp >= C::W_WARP0 && warp < C::EPI_WARP0) {
     // ===== W builders: row r of a cb block, 32 keys per thread (key quarter kq):
-    //       W[m][k] = cb[m][k] exp2(a_m + c_k) for k <= m and k < len, else 0 =====
+    //       W[m][k] = cb[m][k] exp2(a_m - a_{k0}) for k <= m and k < len, else 0 =====
     const int q4 = warp & 3;
     const int kq = (warp - C::W_WARP0) >> 2;  // key quarter of each 128-key block
     const int kh = kq >> 1;                   // the slot (64-key half) it lies in
     const int r = q4 * 32 + lane;             // row within the 128-row tile
     int f = 0, lu = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu, f += C::ITEMS) {
-      int b, c, h;
-      decode(u, b, c, h);
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
+      int b, c, h, mt;
+      decode(u, b, c, h, mt);
       const int len = min(Q, p.L - c * Q);
       const int vb = lu & 1;
       mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
       const float* va = vec + vb * 2 * Q;
       const float* vxs = va + Q;
       // x rows of k-tile kt: x~[k][p] = xs_k x[k][p] in place (row r = key r of the tile; a
-      // SW128 row stays a row, the walk starts at unit r & 7: no bank conflicts). k-tile 0
-      // (needed by the first W.x GEMM) is scaled by key quarter 0 before its W blocks,
-      // k-tile 1 (only the last GEMM) by key quarter 1 after its second block.
+      // SW128 row stays a row, the walk starts at unit r & 7: no bank conflicts). k-tile 0 is
+      // scaled by key quarter 0 first, k-tile 1 (mt = 1 units) by key quarter 1 after its
+      // k-tile 0 W half.
       auto scale_x = [&](int kt) {
-        const int item = kt ? 10 : 5;
+        const int item = kt ? 6 : 3;
         const int s = (f + item) % C::NSLOT;
         mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
         const int k = kt * 128 + r;
@@ -576,25 +588,22 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_xsc(kt));
+        if (lane == 0) mbar_arrive(bar_xsc(lu & 1, kt));
       };
       if (kq == 0) scale_x(0);
-      // blocks (mt, kt, item of this warp's k half)
-      const int blk_mt[3] = {0, 1, 1}, blk_kt[3] = {0, 0, 1};
-      const int blk_it[3] = {6 + kh, 8 + kh, 11 + kh};
-#pragma unroll
-      for (int bi = 0; bi < 3; ++bi) {
-        if (bi == 2 && kq == 1) scale_x(1);
-        const int item = blk_it[bi];
+      const int nblk = mt ? 2 : 1;
+      for (int bi = 0; bi < nblk; ++bi) {  // bi = k-tile of the block
+        if (bi == 1 && kq == 1) scale_x(1);
+        const int item = bi ? 7 + kh : 4 + kh;
         const int s = (f + item) % C::NSLOT;
         mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
         if (r == 0 && (kq & 1) == 0 && lu < 20) SSD_TRACE(1000 + lu * 12 + bi * 4 + kh * 2);
-        const int m = blk_mt[bi] * 128 + r;  // row within the chunk
+        const int m = mt * 128 + r;  // row within the chunk
         const float am = va[m];
         const uint32_t row = sRing + s * SLOT + r * 128;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {  // the thread's two K steps (16 keys each)
-          const int k0 = blk_kt[bi] * 128 + 32 * kq + 16 * ks;
+          const int k0 = bi * 128 + 32 * kq + 16 * ks;
           // W[m][k] = cb[m][k] exp2(a_m - a_{k0}) for k <= m, k < len (x carries xs_k)
           const float sc = (k0 <= m && k0 < len) ? ex2(am - va[k0]) : 0.f;
 #pragma unroll
@@ -625,73 +634,70 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         fence_proxy_async_smem();
         __syncwarp();
         if (r == 0 && (kq & 1) == 0 && lu < 20) SSD_TRACE(1000 + lu * 12 + bi * 4 + kh * 2 + 1);
-        if (lane == 0) mbar_arrive(bar_built(2 * bi + kh));
+        if (lane == 0) mbar_arrive(bar_built(lu & 1, 2 * bi + kh));
       }
+      f += C::items(mt);
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_vec_empty(vb));
     }
   } else if (warp >= C::EPI_WARP0) {
-    // ===== epilogue: out[m][p] = exp(dA[m]) O1 + O2 + D x  (TMEM lane m of each row tile) =====
+    // ===== epilogue: out[m][p] = exp(dA[m]) O1 + O2 + D x  (TMEM lane m of the row tile) =====
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     int lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
-      int b, c, h;
-      decode(u, b, c, h);
-      const int a = lu & 1;
+      int b, c, h, mt;
+      decode(u, b, c, h, mt);
+      const int a = lu % C::NACC;
       const int vb = lu & 1;
       const float Dh = p.D ? p.D[h] : 0.f;
       mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
       const float* va = vec + vb * 2 * Q;
-      mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
+      const int m = mt * 128 + r;
+      const float sm = ex2(va[m]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_vec_empty(vb));  // the vectors are no longer needed
+      mbar_wait(bar_acc_full(a), (lu / C::NACC) & 1);
       if (r == 0 && lu < 20) SSD_TRACE(1600 + lu * 2);
       tc_fence_after();
+      const int t = c * Q + m;
+      const uint32_t tacc = tmem_base + lane_off + a * 128;
+      const size_t ro = (((size_t)b * p.L + t) * p.H + h) * P;  // element offset of row t
+      const bool ok = t < p.L;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int m = mt * 128 + r;
-        const int t = c * Q + m;
-        const float sm = ex2(va[m]);
-        const uint32_t tacc = tmem_base + lane_off + a * 256 + 128 * mt;
-        const size_t ro = (((size_t)b * p.L + t) * p.H + h) * P;  // element offset of row t
-        const bool ok = t < p.L;
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t o1[32], o2[32];
+        tmem_ld32(tacc + cc * 32, o1);
+        tmem_ld32(tacc + 64 + cc * 32, o2);
+        tmem_ld_wait();
+        if (ok) {
+          const uint4* xs = reinterpret_cast<const uint4*>(
+              reinterpret_cast<const uint8_t*>(p.x) + (ro + cc * 32) * 2);
+          uint32_t pk[16];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          uint32_t o1[32], o2[32];
-          tmem_ld32(tacc + cc * 32, o1);
-          tmem_ld32(tacc + 64 + cc * 32, o2);
-          tmem_ld_wait();
-          if (ok) {
-            const uint4* xs = reinterpret_cast<const uint4*>(
-                reinterpret_cast<const uint8_t*>(p.x) + (ro + cc * 32) * 2);
-            uint32_t pk[16];
+          for (int q = 0; q < 4; ++q) {
+            const uint4 xq = __ldg(xs + q);
+            const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 xq = __ldg(xs + q);
-              const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 xf = unpack2<BF16>(xw[e]);
-                const int j = 8 * q + 2 * e;
-                const float y0 = sm * __uint_as_float(o1[j]) + __uint_as_float(o2[j]) + Dh * xf.x;
-                const float y1 = sm * __uint_as_float(o1[j + 1]) + __uint_as_float(o2[j + 1]) + Dh * xf.y;
-                pk[4 * q + e] = pack2rn<BF16>(y0, y1);
-              }
+            for (int e = 0; e < 4; ++e) {
+              const float2 xf = unpack2<BF16>(xw[e]);
+              const int j = 8 * q + 2 * e;
+              const float y0 = sm * __uint_as_float(o1[j]) + __uint_as_float(o2[j]) + Dh * xf.x;
+              const float y1 = sm * __uint_as_float(o1[j + 1]) + __uint_as_float(o2[j + 1]) + Dh * xf.y;
+              pk[4 * q + e] = pack2rn<BF16>(y0, y1);
             }
-            uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) + (ro + cc * 32) * 2;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_global_v4(dst + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           }
+          uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) + (ro + cc * 32) * 2;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            st_global_v4(dst + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (r == 0 && lu < 20) SSD_TRACE(1600 + lu * 2 + 1);
-      if (lane == 0) {
-        mbar_arrive(bar_acc_empty(a));
-        mbar_arrive(bar_vec_empty(vb));
-      }
+      if (lane == 0) mbar_arrive(bar_acc_empty(a));
     }
   }
   tc_fence_before();

@@ -954,7 +954,10 @@ int ssd_launch(K kern, int smem, int threads, const ssd::SsdParams& prm, DeviceI
       di.smem_set[inst] = true;
     }
   }
-  const int grid = prm.n_units < di.sm_count ? prm.n_units : di.sm_count;
+  // persistent CTAs striding over units; an odd grid makes each CTA alternate the unit
+  // kinds of chunk_scan (units 2i / 2i+1 are the light / heavy row tile of one (b, c, h))
+  int grid = prm.n_units < di.sm_count ? prm.n_units : di.sm_count;
+  if (grid > 1 && grid % 2 == 0 && grid < prm.n_units) --grid;
   kern<<<grid, threads, smem, stream>>>(prm);
   if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
   return TL_OK;
@@ -1046,7 +1049,7 @@ extern "C" int tl_ssd_chunk_scan(const void* cb, const void* x, const float* dt,
   prm.G = ngroups;
   prm.nc = nc;
   prm.grp = nheads / ngroups;
-  prm.n_units = batch * nc * nheads;
+  prm.n_units = batch * nc * nheads * 2;  // (b, c, h, 128-row tile)
   prm.trace = g_trace;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   rc = dtype == TL_DTYPE_BF16
