@@ -327,6 +327,15 @@ def run_ours(args, world, rank, local):
                            else f"tl_attn_fwd_kernel<{cfg.D},{cfg.dtype_name}>"),
                 "frac_of_sustained": achieved / pk["sustained"],
                 "frac_of_spec_2250": achieved / 2250.0}
+    # the softmax's own floor: every allowed (query, key) pair needs one exp2,
+    # 16 per clock per SM on MUFU, at the median SM clock measured during the timed region
+    ck = clk.summary()
+    mhz = ck.get("sm_mhz") or ck.get("sm_max_mhz")
+    if mhz:
+        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        floor_ms = cfg.flops_exact() / world / (4.0 * cfg.D) / (n_sm * 16 * mhz * 1e6) * 1e3
+        roofline["mufu_floor_ms"] = floor_ms
+        roofline["frac_of_mufu_floor"] = floor_ms / kern_ms
 
     gather_ms = None
     if args.gather and world > 1:
@@ -394,8 +403,9 @@ def run_ours(args, world, rank, local):
                 continue
             extra[name] = bench_one(CONFIGS[name], pk, steps=max(5, min(args.steps, 20)))
         from paper_2504_17577_b200.configs import PAPER_T3
-        for name in ("FA3", "FA4"):  # the paper's own FlashAttention shapes (Table 3)
-            extra["paper_" + name] = bench_one(PAPER_T3[name], pk, steps=max(5, min(args.steps, 20)))
+        for name in ("FA0", "FA1", "FA2", "FA3", "FA4"):  # the paper's FlashAttention shapes (Table 3)
+            extra["paper_" + name] = bench_one(PAPER_T3[name], pk, steps=max(5, min(args.steps, 20)),
+                                               graph=True)
         for gname in ("M5", "M2", "V1", "V4"):  # the paper's GEMM on Table 2 shapes
             extra["gemm_" + gname] = bench_gemm(gname, pk)
         from paper_2504_17577_b200.configs import MLA_CONFIGS
@@ -463,7 +473,7 @@ def ncu_traffic(name, world):
         return None
 
 
-def bench_one(cfg, pk, steps=20, warmup=3):
+def bench_one(cfg, pk, steps=20, warmup=3, graph=False):
     from paper_2504_17577_b200 import attention
     from paper_2504_17577_b200.inputs import gen_qkv
     q, k, v = gen_qkv(cfg.B, cfg.Hq, cfg.Hkv, cfg.Sq, cfg.Skv, cfg.D, cfg.dtype, cfg.seed, "cuda")
@@ -479,21 +489,57 @@ def bench_one(cfg, pk, steps=20, warmup=3):
         call()
     st = torch.cuda.current_stream()
     evs = []
-    for _ in range(steps):
-        if flush is not None:
-            flush.zero_()  # write > L2 between launches for L2-resident shapes
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        call()
-        b.record(st)
-        evs.append((a, b))
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device(), period=0.002) as clk:
+        for _ in range(steps):
+            if flush is not None:
+                flush.zero_()  # write > L2 between launches for L2-resident shapes
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            call()
+            b.record(st)
+            evs.append((a, b))
+        torch.cuda.synchronize()
     kern_ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
     tf = cfg.flops() / (kern_ms * 1e-3) / 1e12
     res = {"tflops": tf, "kernel_ms": kern_ms, "frac_of_peak": tf / pk["burst"],
            "hbm_gbs": cfg.hbm_bytes() / (kern_ms * 1e-3) / 1e9, **cfg.as_dict()}
+    # MUFU-only softmax floor: one exp2 per allowed (query, key) pair at 16 ex2 / clock / SM
+    # (the SFU rate, B200_PROFILING / r02 notes) and the median SM clock of this run
+    ck = clk.summary()
+    mhz = ck.get("sm_mhz") or ck.get("sm_max_mhz")
+    if mhz:
+        n_exp = cfg.flops_exact() / (4.0 * cfg.D)
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        floor_ms = n_exp / (n_sm * 16 * mhz * 1e6) * 1e3
+        res.update({"mufu_floor_ms": floor_ms, "frac_of_mufu_floor": floor_ms / kern_ms,
+                    "mufu_floor_clock_mhz": mhz})
     if small:
         res["note"] = "L2 flushed between launches (256 MB write)"
+    if graph:
+        # device time per launch without host launch cost: 20 back-to-back calls in one CUDA
+        # graph (inputs L2-warm), replayed 5 times
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(st)
+        with torch.cuda.stream(s_):
+            call()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s_):
+            for _ in range(20):
+                call()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(5):
+            g.replay()
+        b.record(st)
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b) / 100
+        res["graph_us"] = gms * 1e3
+        res["graph_tflops"] = cfg.flops() / (gms * 1e-3) / 1e12
+        res["graph_note"] = "CUDA graph of 20 back-to-back launches, L2-warm, device time per launch"
+        del g
     del q, k, v, o, lse
     torch.cuda.empty_cache()
     return res

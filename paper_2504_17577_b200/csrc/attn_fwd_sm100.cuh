@@ -139,7 +139,15 @@ __device__ __forceinline__ int n_outputs(const PT& p) {
   do {                                                                                   \
     if (p.trace != nullptr) p.trace[16000 + 16 * blockIdx.x + (idx)] = globaltimer();    \
   } while (0)
+// second per-CTA area (producer events of the first unit)
+#define TL_SPAN2(idx)                                                                      \
+  do {                                                                                     \
+    if (p.trace != nullptr) p.trace[16000 + 16 * 160 + 16 * blockIdx.x + (idx)] = globaltimer(); \
+  } while (0)
 #else
+#define TL_SPAN2(idx) \
+  do {                \
+  } while (0)
 #define TL_SPAN(idx) \
   do {               \
   } while (0)

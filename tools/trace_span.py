@@ -21,7 +21,7 @@ def main():
         cfg = ALL[name]
         lib = load_library()
         lib.tl_attn_debug_trace.argtypes = [ctypes.c_void_p]
-        buf = torch.zeros(16000 + 16 * 160, dtype=torch.int64, device="cuda")
+        buf = torch.zeros(16000 + 32 * 160, dtype=torch.int64, device="cuda")
         q, k, v = gen_qkv(cfg.B, cfg.Hq, cfg.Hkv, cfg.Sq, cfg.Skv, cfg.D, cfg.dtype, cfg.seed, "cuda")
         o = torch.empty_like(q)
         f = lambda: attention(q, k, v, causal=cfg.causal, scale=cfg.scale, out=o)  # noqa: E731
@@ -37,14 +37,21 @@ def main():
             f()
             b.record()
             torch.cuda.synchronize()
-            sp = buf[16000:].view(160, 16).cpu().numpy().astype(np.int64)
+            sp = buf[16000:16000 + 16 * 160].view(160, 16).cpu().numpy().astype(np.int64)
+            pr = buf[16000 + 16 * 160:].view(160, 16).cpu().numpy().astype(np.int64)
             live = sp[:, 0] > 0
-            sp = sp[live]
+            sp, pr = sp[live], pr[live]
             t0 = sp[:, 0].min()
+            prel = np.where(pr > 0, pr - t0, -1) / 1000.0
+            names = ["Q0 issue", "Q0 issued", "ring0", "ring1", "ring2", "ring3", "ring4", "ring5", "producer start"]
+            print("  producer (median us): " + ", ".join(
+                f"{names[i]} {np.median(prel[prel[:, i] >= 0, i]):.2f}" for i in (8, 0, 1, 2, 3, 4, 5, 6, 7)
+                if (prel[:, i] >= 0).any()))
             rel = np.where(sp > 0, sp - t0, -1) / 1000.0  # us
             print(f"== {name} {'cold L2' if cold else 'warm L2'}: event {a.elapsed_time(b) * 1e3:.1f} us, "
                   f"{len(sp)} CTAs")
-            print(f"  entry spread  {rel[:, 0].max():.2f} us")
+            print(f"  entry spread  {rel[:, 0].max():.2f} us; setup done median {np.median(rel[:, 14]):.2f}; "
+                  f"leader Q ready median {np.median(rel[rel[:, 13] >= 0, 13]):.2f}")
             for kk in range(4):
                 s, e = rel[:, 1 + 3 * kk], rel[:, 2 + 3 * kk]
                 ok = (s >= 0) & (e >= 0)
