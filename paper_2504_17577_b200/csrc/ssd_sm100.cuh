@@ -14,7 +14,8 @@
 // goal is to stream x / states / out at HBM speed with the contraction on tcgen05.
 //
 // B200 design (single-CTA tcgen05, M = 128; persistent CTAs striding over units):
-//   * chunk_state unit = (b, c, head pair): A = x'^T [M = 2 heads x 64 p][K = Q positions]
+//   * chunk_state unit = (b, c, 4 heads, or a head pair when the group size is not a multiple
+//     of 4): per head pair A = x'^T [M = 2 heads x 64 p][K = Q positions]
 //     with x' = w[i] x (each x row scaled in SMEM by "scale" warps: the TMA box [64 t][64 p]
 //     is exactly the MN-major SWIZZLE_128B A operand, a row stays a row under the swizzle),
 //     B = Bm [N = 128 n][K] (MN-major), D = states in TMEM (double-buffered over units), the
@@ -100,24 +101,37 @@ __device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t (&r)[4]) {
 }
 
 // ============================================================================ chunk_state
+// Unit = (b, c, HU heads of one group). HU = 4 when the group size allows it: the unit's Bm
+// tile (16 KB per 64-position stage) then serves four heads, so SMEM ingress per head is
+// x 32 KB + Bm 16 KB = the head's own HBM bytes (x in, states out), where head pairs pulled
+// 64 KB per head from L2 (the Bm copy of every pair). Two M = 128 accumulators (heads 0-1,
+// 2-3) per unit; HU = 2 keeps the one-tile form.
+template <int HU>
 struct StateCfg {
-  static constexpr int NSLOT = 12;                  // 16 KB slots (a stage = 2 slots)
+  static_assert(HU == 2 || HU == 4, "heads per unit");
+  static constexpr int NT = HU / 2;                 // M = 128 tiles (head pairs) per unit
+  static constexpr int NSLOT = 12;                  // 16 KB slots
+  static constexpr int STAGE_SLOTS = NT + 1;        // x of HU heads (8 KB each) + Bm (16 KB)
+  static constexpr int STAGE_BYTES = STAGE_SLOTS * SLOT;
+  static constexpr int NST = NSLOT / STAGE_SLOTS;   // stages in flight (6 / 4)
   static constexpr int STAGES = Q / 64;             // 64 positions per stage
   static constexpr int OFF_RING = 0;
-  static constexpr int OFF_BAR = OFF_RING + NSLOT * SLOT;
-  // full[NSLOT/2] scaled[NSLOT/2] empty[NSLOT/2] acc_full[2] acc_empty[2]
-  static constexpr int NST = NSLOT / 2;             // stages in flight
+  static constexpr int OFF_BAR = OFF_RING + NST * STAGE_BYTES;
+  // full[NST] scaled[NST] empty[NST] acc_full[2] acc_empty[2]
   static constexpr int NUM_BARS = 3 * NST + 4;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
-  static constexpr int THREADS = 384;  // 0 TMA, 1 MMA, 4-7 scale, 8-11 epilogue
+  static constexpr int SCALE_WARPS = 2 * HU;        // one x row (position, head) per thread
+  static constexpr int EPI_WARP0 = 4 + SCALE_WARPS;
+  static constexpr int THREADS = (EPI_WARP0 + 4) * 32;  // 0 TMA, 1 MMA, scale, 4 epilogue
+  static constexpr int TMEM_COLS = 2 * NT * N;      // double-buffered over units
   static_assert(SMEM_BYTES <= 232448, "shared memory budget exceeded");
 };
 
-template <bool BF16>
-__global__ void __launch_bounds__(StateCfg::THREADS, 1)
+template <bool BF16, int HU>
+__global__ void __launch_bounds__(StateCfg<HU>::THREADS, 1)
 tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
-  using C = StateCfg;
+  using C = StateCfg<HU>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   if ((base & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1024-B alignment
@@ -131,14 +145,14 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int H2 = p.H >> 1;
+  const int HG = p.H / HU;  // head groups of HU heads
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tm_x);
     prefetch_tmap(&p.tm_b);
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(bar_full(s), 1);
-      mbar_init(bar_scaled(s), 4);
+      mbar_init(bar_scaled(s), C::SCALE_WARPS);
       mbar_init(bar_empty(s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -147,16 +161,16 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<256>(smem_u32(tmem_ptr_smem));
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(smem_u32(tmem_ptr_smem));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_smem;
 
-  // unit u -> (b, c, head pair hp); consecutive units share (b, c): Bm of the chunk from L2
-  auto decode = [&](int u, int& b, int& c, int& hp) {
-    hp = u % H2;
-    const int bc = u / H2;
+  // unit u -> (b, c, head group hg); consecutive units share (b, c): Bm of the chunk from L2
+  auto decode = [&](int u, int& b, int& c, int& hg) {
+    hg = u % HG;
+    const int bc = u / HG;
     c = bc % p.nc;
     b = bc / p.nc;
   };
@@ -168,21 +182,22 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       const uint64_t pol_b = policy_evict_last();
       int it = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        int b, c, hp;
-        decode(u, b, c, hp);
-        const int h0 = 2 * hp, g = h0 / p.grp;
+        int b, c, hg;
+        decode(u, b, c, hg);
+        const int h0 = HU * hg, g = h0 / p.grp;
         for (int st = 0; st < C::STAGES; ++st, ++it) {
           const int s = it % C::NST;
           if (it >= C::NST) mbar_wait(bar_empty(s), ((it / C::NST) - 1) & 1);
-          mbar_arrive_expect_tx(bar_full(s), 2 * SLOT);
+          mbar_arrive_expect_tx(bar_full(s), C::STAGE_BYTES);
           SSD_TRACE(it * 4 + 0);
-          const uint32_t dst = sRing + s * 2 * SLOT;
+          const uint32_t dst = sRing + s * C::STAGE_BYTES;
           const int t0 = c * Q + st * 64;
-          // x rows [t0, t0+64) of heads h0, h0+1 (OOB rows past L zero-filled), then Bm
-          tma_load_4d(dst, &p.tm_x, bar_full(s), 0, h0, t0, b, pol_x);
-          tma_load_4d(dst + 8192, &p.tm_x, bar_full(s), 0, h0 + 1, t0, b, pol_x);
-          tma_load_4d(dst + SLOT, &p.tm_b, bar_full(s), 0, g, t0, b, pol_b);
-          tma_load_4d(dst + SLOT + 8192, &p.tm_b, bar_full(s), 64, g, t0, b, pol_b);
+          // x rows [t0, t0+64) of heads h0 .. h0+HU-1 (OOB rows past L zero-filled), then Bm
+#pragma unroll
+          for (int hh = 0; hh < HU; ++hh)
+            tma_load_4d(dst + hh * 8192, &p.tm_x, bar_full(s), 0, h0 + hh, t0, b, pol_x);
+          tma_load_4d(dst + HU * 8192, &p.tm_b, bar_full(s), 0, g, t0, b, pol_b);
+          tma_load_4d(dst + HU * 8192 + 8192, &p.tm_b, bar_full(s), 64, g, t0, b, pol_b);
         }
       }
     }
@@ -197,25 +212,29 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       const int a = lu & 1;
       if (lu >= 2) mbar_wait(bar_acc_empty(a), ((lu >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t tm_d = tmem_base + a * N;
       for (int st = 0; st < C::STAGES; ++st, ++it) {
         const int s = it % C::NST;
         mbar_wait(bar_scaled(s), (it / C::NST) & 1);
         if (lane == 0) SSD_TRACE(it * 4 + 2);
         tc_fence_after();
-        const uint32_t xa = sRing + s * 2 * SLOT;
+        const uint32_t xa = sRing + s * C::STAGE_BYTES;
+        const uint32_t ba = xa + HU * 8192;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // 16 positions per K step: +16 rows of 128 B
-          if (elect_one())
-            mma_f16_ss(tm_d, make_sdesc_sw128(xa + kk * 2048, 8192, 1024),
-                       make_sdesc_sw128(xa + SLOT + kk * 2048, 8192, 1024), IDESC,
-                       (st > 0 || kk > 0) ? 1u : 0u);
+        for (int mt = 0; mt < C::NT; ++mt) {  // heads 2mt, 2mt+1: two 64-wide MN atoms
+          const uint32_t tm_d = tmem_base + (a * C::NT + mt) * N;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // 16 positions per K step: +16 rows of 128 B
+            if (elect_one())
+              mma_f16_ss(tm_d, make_sdesc_sw128(xa + mt * 16384 + kk * 2048, 8192, 1024),
+                         make_sdesc_sw128(ba + kk * 2048, 8192, 1024), IDESC,
+                         (st > 0 || kk > 0) ? 1u : 0u);
+        }
         if (elect_one()) mma_commit(bar_empty(s));
       }
       if (elect_one()) mma_commit(bar_acc_full(a));
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < C::EPI_WARP0) {
     // ===== scale warps: x row (t, head) *= w[t] = exp(dA[last] - dA[t]) dt[t], in SMEM =====
     const int i = threadIdx.x - 128;
     const int r = i & 63, hh = i >> 6;
@@ -227,9 +246,9 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
     };
     auto load_raw = [&](int u) {
       Raw v;
-      int b, c, hp;
-      decode(u, b, c, hp);
-      const int h = 2 * hp + hh;
+      int b, c, hg;
+      decode(u, b, c, hg);
+      const int h = HU * hg + hh;
       v.len = min(Q, p.L - c * Q);
       const size_t vo = ((size_t)(b * p.H + h) * p.nc + c) * Q;
       v.last = __ldg(p.dA + vo + v.len - 1);
@@ -254,7 +273,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
         // row r of box hh: 128 B (a SW128 row stays one row; only its 16-B units permute).
         // Thread r walks the units starting at r & 7, so the 8 threads of a quarter-warp
         // (rows r..r+7, 128 B apart) hit 8 different bank groups (no 8-way conflict).
-        const uint32_t row = sRing + s * 2 * SLOT + hh * 8192 + r * 128;
+        const uint32_t row = sRing + s * C::STAGE_BYTES + hh * 8192 + r * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const uint32_t addr = row + ((q ^ (r & 7)) << 4);
@@ -273,34 +292,38 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
       }
       cur = nxt;
     }
-  } else if (warp >= 8) {
-    // ===== epilogue: TMEM lane m = (head h0 + m/64, p = m%64) -> 128 states, RN, global =====
+  } else if (warp >= C::EPI_WARP0) {
+    // ===== epilogue: TMEM lane m of tile mt = (head h0 + 2 mt + m/64, p = m%64) -> 128
+    //       states, RN, global =====
     const int q4 = warp & 3;
     const int m = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     int lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
-      int b, c, hp;
-      decode(u, b, c, hp);
+      int b, c, hg;
+      decode(u, b, c, hg);
       const int a = lu & 1;
-      const int h = 2 * hp + (m >> 6), pp = m & 63;
       mbar_wait(bar_acc_full(a), (lu >> 1) & 1);
       if (m == 0) SSD_TRACE(2000 + lu * 2);
       tc_fence_after();
-      uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) +
-                     ((((size_t)b * p.nc + c) * p.H + h) * P + pp) * (size_t)N * 2;
+#pragma unroll 1
+      for (int mt = 0; mt < C::NT; ++mt) {
+        const int h = HU * hg + 2 * mt + (m >> 6), pp = m & 63;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(p.out) +
+                       ((((size_t)b * p.nc + c) * p.H + h) * P + pp) * (size_t)N * 2;
 #pragma unroll
-      for (int cc = 0; cc < N / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + lane_off + a * N + cc * 32, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
+        for (int cc = 0; cc < N / 32; ++cc) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + lane_off + (a * C::NT + mt) * N + cc * 32, v);
+          tmem_ld_wait();
+          uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = pack2rn<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+          for (int e = 0; e < 16; ++e)
+            pk[e] = pack2rn<BF16>(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          st_global_v4(dst + cc * 64 + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          for (int q = 0; q < 4; ++q)
+            st_global_v4(dst + cc * 64 + q * 16, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -312,7 +335,7 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem_base);
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -422,8 +445,19 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   if (warp == 0) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-      const uint64_t pol_s = policy_evict_first();   // prev: read by the 2 row-tile units
-      const uint64_t pol_l = policy_evict_last();    // C, cb, x: re-read by other units
+#ifdef TLATTN_SCAN_POL_NEW
+      // C, cb: shared by every head of the group (re-read by up to 2 x grp units) -> keep;
+      // prev, x: re-read only by the neighbouring row-tile unit and this unit's epilogue ->
+      // normal priority (an evict_last x, 4.3 GB at CC5, crowded the L2 and cost ~3.8 GB of
+      // HBM re-reads per launch in ncu)
+      const uint64_t pol_s = policy_evict_normal();
+      const uint64_t pol_x = policy_evict_normal();
+      const uint64_t pol_l = policy_evict_last();
+#else
+      const uint64_t pol_s = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_l = policy_evict_last();
+#endif
       int f = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         int b, c, h, mt;
@@ -447,7 +481,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
               tma_load_4d(dst, &p.tm_c, fb, 64 * (item - 1), g, c * Q + 128 * mt, b, pol_l);
               break;
             case 3: case 6:  // x [128 k][64 p] of k-tile 0 / 1
-              tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * (item == 6), b, pol_l);
+              tma_load_4d(dst, &p.tm_x, fb, 0, h, c * Q + 128 * (item == 6), b, pol_x);
               break;
             default: {  // cb [128 m][64 k]: items 4,5 (k-tile 0), 7,8 (k-tile 1)
               const int kt = item >= 7, kh = (item == 5 || item == 8);

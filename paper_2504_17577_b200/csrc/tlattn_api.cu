@@ -997,12 +997,22 @@ extern "C" int tl_ssd_chunk_state(const void* x, const void* Bm, const float* dt
   prm.G = ngroups;
   prm.nc = (seqlen + chunk_size - 1) / chunk_size;
   prm.grp = nheads / ngroups;
-  prm.n_units = batch * prm.nc * (nheads / 2);
   prm.trace = g_trace;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  rc = dtype == TL_DTYPE_BF16
-           ? ssd_launch(ssd::tl_ssd_state_kernel<true>, ssd::StateCfg::SMEM_BYTES, ssd::StateCfg::THREADS, prm, *di, 18, st)
-           : ssd_launch(ssd::tl_ssd_state_kernel<false>, ssd::StateCfg::SMEM_BYTES, ssd::StateCfg::THREADS, prm, *di, 19, st);
+  // four heads per unit (one Bm tile for four heads) when they share a group
+  using S2 = ssd::StateCfg<2>;
+  using S4 = ssd::StateCfg<4>;
+  if ((nheads / ngroups) % 4 == 0) {
+    prm.n_units = batch * prm.nc * (nheads / 4);
+    rc = dtype == TL_DTYPE_BF16
+             ? ssd_launch(ssd::tl_ssd_state_kernel<true, 4>, S4::SMEM_BYTES, S4::THREADS, prm, *di, 22, st)
+             : ssd_launch(ssd::tl_ssd_state_kernel<false, 4>, S4::SMEM_BYTES, S4::THREADS, prm, *di, 23, st);
+  } else {
+    prm.n_units = batch * prm.nc * (nheads / 2);
+    rc = dtype == TL_DTYPE_BF16
+             ? ssd_launch(ssd::tl_ssd_state_kernel<true, 2>, S2::SMEM_BYTES, S2::THREADS, prm, *di, 18, st)
+             : ssd_launch(ssd::tl_ssd_state_kernel<false, 2>, S2::SMEM_BYTES, S2::THREADS, prm, *di, 19, st);
+  }
   if (rc == TL_OK) g_last_launches = 1;
   return rc;
 }

@@ -65,6 +65,7 @@ SMALL = [  # B, L, H, G, dtype
     (1, 700, 6, 3, F16),    # three chunks, the last partial
     (1, 100, 2, 1, BF),     # one partial chunk (second row tile empty)
     (3, 512, 8, 1, F16),
+    (2, 1100, 12, 3, BF),   # groups of 4 heads (four-head state units), ragged, 5 chunks
 ]
 
 
