@@ -445,11 +445,11 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   if (warp == 0) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-#ifdef TLATTN_SCAN_POL_NEW
+#ifndef TLATTN_SCAN_POL_OLD
       // C, cb: shared by every head of the group (re-read by up to 2 x grp units) -> keep;
       // prev, x: re-read only by the neighbouring row-tile unit and this unit's epilogue ->
-      // normal priority (an evict_last x, 4.3 GB at CC5, crowded the L2 and cost ~3.8 GB of
-      // HBM re-reads per launch in ncu)
+      // normal priority (with x evict_last, 4.3 GB at CC5, ncu counted 11.1 GB of DRAM reads
+      // per launch, 9.9 GB with this policy; CC5 -1 %)
       const uint64_t pol_s = policy_evict_normal();
       const uint64_t pol_x = policy_evict_normal();
       const uint64_t pol_l = policy_evict_last();
