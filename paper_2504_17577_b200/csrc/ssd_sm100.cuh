@@ -26,8 +26,9 @@
 //     the decay split per MMA K step of 16 keys: exp(dA_m - dA_k) dt_k =
 //     exp2(a_m - a_{k0(k)}) * [dt_k exp2(a_{k0(k)} - a_k)] with a = dA log2 e; the second
 //     (bounded) factor scales the x rows, the first (one exp per row and K step) the cb tile:
-//     W = cb exp2(a_m - a_k0) [k <= m], built in SMEM by 16 "W" warps (one row per thread,
-//     four threads per row: 32 keys each); the causal structure skips the (m0, k1) block.
+//     W = cb exp2(a_m - a_k0) [k <= m], built by 16 "W" warps (one row per thread, four
+//     threads per row: 32 keys each) from the cb tile in SMEM straight into TMEM, where it is
+//     the A operand of the W . x MMAs; the causal structure skips the (m0, k1) block.
 //     The epilogue warps form out = exp(dA[m]) O1 + O2 + D x.
 //   * every operand streams through one ring of 16 KB TMA slots (per-slot full / empty
 //     barriers; the six W half-blocks of a unit also have "built" barriers) in one fixed
@@ -353,20 +354,25 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
 // alternates the lighter mt = 0 and the heavier mt = 1 units.
 struct ScanCfg {
   static constexpr int NSLOT = 12;
-  static constexpr int NACC = 4;  // TMEM accumulator buffers (O1 | O2: 128 columns each)
+  static constexpr int NACC = 2;  // TMEM accumulator buffers (O1 | O2: 128 columns each)
+  // W lives in TMEM as the A operand of the W . x~ MMAs (tcgen05 "ts" form): two sets (unit
+  // parity) x two blocks x 64 columns (128 keys as bf16 pairs) from column 256 — the MMAs then
+  // read only x~ from SMEM (2 KB per MMA instead of 6 KB) and the W warps write no SMEM
+  static constexpr uint32_t TM_W = NACC * 128;
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // a, xs of the unit: 2 x Q f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * Q * 4;   // double-buffered over units
   // full[NSLOT] empty[NSLOT] built[2][4] acc_full[NACC] acc_empty[NACC] vec_full[2]
-  // vec_empty[2] xsc[2][2]. built[set][2 * block + k half] (block 0 = the k-tile 0 W block;
-  // block 1 = the diagonal block of a mt = 1 unit) and xsc[set][kt] belong to the unit's
+  // vec_empty[2] xsc[2][2] wfree[2] (W TMEM set free: the unit's W . x~ MMAs completed).
+  // built[set][2 * block + k half] (block 0 = the k-tile 0 W block; block 1 = the diagonal
+  // block of a mt = 1 unit), xsc[set][kt] and wfree[set] belong to the unit's
   // parity set = lu & 1 and complete once per unit that uses them (units alternate mt, so a
   // set's barriers see one phase per use: wait parity (lu >> 1) & 1). Two sets let the W
   // warps run one unit ahead of the MMA; they cannot run two ahead because that unit's cb
   // slots are only refilled after the MMA released this unit's. (A per-slot "built" barrier
   // would complete only on that slot's W fills and fall out of step with the fill-count
   // parity its waiters follow.)
-  static constexpr int NUM_BARS = 2 * NSLOT + 8 + 2 * NACC + 4 + 4;
+  static constexpr int NUM_BARS = 2 * NSLOT + 8 + 2 * NACC + 4 + 4 + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
   // warps: 0 TMA, 1 MMA, 2 unit vectors, 4-19 W builders (4 key quarters x 4 lane
@@ -398,6 +404,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   auto bar_xsc = [&](int set, int kt) {
     return bar0 + 8u * (2 * C::NSLOT + 12 + 2 * C::NACC + 2 * set + kt);
   };
+  auto bar_wfree = [&](int set) { return bar0 + 8u * (2 * C::NSLOT + 16 + 2 * C::NACC + set); };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -414,6 +421,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     for (int set = 0; set < 2; ++set) {
       for (int w = 0; w < 4; ++w) mbar_init(bar_built(set, w), 8);  // 8 W warps of a k half
       for (int kt = 0; kt < 2; ++kt) mbar_init(bar_xsc(set, kt), 4);  // one lane-quarter group
+      mbar_init(bar_wfree(set), 1);  // MMA commit
     }
     for (int i = 0; i < C::NACC; ++i) {
       mbar_init(bar_acc_full(i), 1);
@@ -536,22 +544,28 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         mbar_wait(bar_built(set, 2 * wblk), upar);
         mbar_wait(bar_built(set, 2 * wblk + 1), upar);
         tc_fence_after();
+        // the cb slots were read (into W in TMEM) by the W warps: free them now
+        if (elect_one()) {
+          mbar_arrive(bar_empty(slot(wa)));
+          mbar_arrive(bar_empty(slot(wb)));
+        }
+        const uint32_t wt = tmem_base + C::TM_W + set * 128 + wblk * 64;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t asrc = saddr(kk < 4 ? wa : wb) + (kk & 3) * 32;
+        for (int kk = 0; kk < 8; ++kk) {  // A = W in TMEM: 16 keys = 8 columns
           const uint32_t bsrc = saddr(xi) + kk * 2048;
           if (elect_one())
-            mma_f16_ss(acc + 64, make_sdesc_sw128(asrc, 16, 1024),
-                       make_sdesc_sw128(bsrc, 16, 1024), IDESC2, (!first || kk > 0) ? 1u : 0u);
+            mma_f16_ts(acc + 64, wt + kk * 8, make_sdesc_sw128(bsrc, 16, 1024), IDESC2,
+                       (!first || kk > 0) ? 1u : 0u);
         }
       };
       gemm2(0, 4, 5, 3, 0, true);
-      release(3), release(4), release(5);
+      release(3);
       if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 2);
       if (mt) {
         gemm2(1, 7, 8, 6, 1, false);
-        release(6), release(7), release(8);
+        release(6);
       }
+      if (elect_one()) mma_commit(bar_wfree(set));  // this unit's W TMEM set read
       if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 3);
       if (elect_one()) mma_commit(bar_acc_full(a));
       f += C::items(mt);
@@ -625,6 +639,9 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         if (lane == 0) mbar_arrive(bar_xsc(lu & 1, kt));
       };
       if (kq == 0) scale_x(0);
+      // this unit's W TMEM set (lu & 1) was read by the MMAs of unit lu - 2
+      if (lu >= 2) mbar_wait(bar_wfree(lu & 1), ((lu >> 1) - 1) & 1);
+      tc_fence_after();
       const int nblk = mt ? 2 : 1;
       for (int bi = 0; bi < nblk; ++bi) {  // bi = k-tile of the block
         if (bi == 1 && kq == 1) scale_x(1);
@@ -635,6 +652,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         const int m = mt * 128 + r;  // row within the chunk
         const float am = va[m];
         const uint32_t row = sRing + s * SLOT + r * 128;
+        uint32_t wv[16];  // this thread's 32 keys of W row m, bf16 pairs in key order
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {  // the thread's two K steps (16 keys each)
           const int k0 = bi * 128 + 32 * kq + 16 * ks;
@@ -662,10 +680,16 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
                 v[e] = pack2rn<BF16>(w0, w1);
               }
             }
-            st_shared_v4(addr, v[0], v[1], v[2], v[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) wv[8 * ks + 4 * hh + e] = v[e];
           }
         }
-        fence_proxy_async_smem();
+        // W row m, keys [32 kq, 32 kq + 32) of the block -> TMEM lane r, 16 columns
+        tmem_st16(tmem_base + (static_cast<uint32_t>(q4 * 32) << 16) + C::TM_W + (lu & 1) * 128 +
+                      bi * 64 + kq * 16,
+                  wv);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
         if (r == 0 && (kq & 1) == 0 && lu < 20) SSD_TRACE(1000 + lu * 12 + bi * 4 + kh * 2 + 1);
         if (lane == 0) mbar_arrive(bar_built(lu & 1, 2 * bi + kh));
