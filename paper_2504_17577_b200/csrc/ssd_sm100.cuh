@@ -24,11 +24,12 @@
 //   * chunk_scan unit = (b, c, h, row tile of 128): O1 = C [m][n] . prev [p][n]^T
 //     (both K-major, K = n = 128), O2 = W [m][k] . x [k][p] (x MN-major, K = k) with
 //     the decay split per MMA K step of 16 keys: exp(dA_m - dA_k) dt_k =
-//     exp2(a_m - a_{k0(k)}) * [dt_k exp2(a_{k0(k)} - a_k)] with a = dA log2 e; the second
-//     (bounded) factor scales the x rows, the first (one exp per row and K step) the cb tile:
-//     W = cb exp2(a_m - a_k0) [k <= m], built by 16 "W" warps (one row per thread, four
-//     threads per row: 32 keys each) from the cb tile in SMEM straight into TMEM, where it is
-//     the A operand of the W . x MMAs; the causal structure skips the (m0, k1) block.
+//     exp2(a_m - a_{k0(k)}) * xs_k, xs_k = dt_k exp2(a_{k0(k)} - a_k), a = dA log2 e: ONE
+//     exp per row and K step (the first factor) and one multiply per element by the per-key
+//     xs_k: W = cb exp2(a_m - a_k0) xs_k [k <= m], built by 16 "W" warps (one row per thread,
+//     four threads per row: 32 keys each) from the cb tile in SMEM straight into TMEM, where
+//     it is the A operand of the W . x MMAs (x stays as loaded); the causal structure skips
+//     the (m0, k1) block.
 //     The epilogue warps form out = exp(dA[m]) O1 + O2 + D x.
 //   * every operand streams through one ring of 16 KB TMA slots (per-slot full / empty
 //     barriers; the six W half-blocks of a unit also have "built" barriers) in one fixed
@@ -355,24 +356,24 @@ tl_ssd_state_kernel(const __grid_constant__ SsdParams p) {
 struct ScanCfg {
   static constexpr int NSLOT = 12;
   static constexpr int NACC = 2;  // TMEM accumulator buffers (O1 | O2: 128 columns each)
-  // W lives in TMEM as the A operand of the W . x~ MMAs (tcgen05 "ts" form): two sets (unit
+  // W lives in TMEM as the A operand of the W . x MMAs (tcgen05 "ts" form): two sets (unit
   // parity) x two blocks x 64 columns (128 keys as bf16 pairs) from column 256 — the MMAs then
-  // read only x~ from SMEM (2 KB per MMA instead of 6 KB) and the W warps write no SMEM
+  // read only x from SMEM (2 KB per MMA instead of 6 KB) and the W warps write no SMEM
   static constexpr uint32_t TM_W = NACC * 128;
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_VEC = OFF_RING + NSLOT * SLOT;   // a, xs of the unit: 2 x Q f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * Q * 4;   // double-buffered over units
   // full[NSLOT] empty[NSLOT] built[2][4] acc_full[NACC] acc_empty[NACC] vec_full[2]
-  // vec_empty[2] xsc[2][2] wfree[2] (W TMEM set free: the unit's W . x~ MMAs completed).
+  // vec_empty[2] wfree[2] (W TMEM set free: the unit's W . x MMAs completed).
   // built[set][2 * block + k half] (block 0 = the k-tile 0 W block; block 1 = the diagonal
-  // block of a mt = 1 unit), xsc[set][kt] and wfree[set] belong to the unit's
+  // block of a mt = 1 unit) and wfree[set] belong to the unit's
   // parity set = lu & 1 and complete once per unit that uses them (units alternate mt, so a
   // set's barriers see one phase per use: wait parity (lu >> 1) & 1). Two sets let the W
   // warps run one unit ahead of the MMA; they cannot run two ahead because that unit's cb
   // slots are only refilled after the MMA released this unit's. (A per-slot "built" barrier
   // would complete only on that slot's W fills and fall out of step with the fill-count
   // parity its waiters follow.)
-  static constexpr int NUM_BARS = 2 * NSLOT + 8 + 2 * NACC + 4 + 4 + 2;
+  static constexpr int NUM_BARS = 2 * NSLOT + 8 + 2 * NACC + 4 + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NUM_BARS * 8;
   static constexpr int SMEM_BYTES = OFF_TMEMPTR + 16;
   // warps: 0 TMA, 1 MMA, 2 unit vectors, 4-19 W builders (4 key quarters x 4 lane
@@ -401,10 +402,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
   auto bar_acc_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + C::NACC + i); };
   auto bar_vec_full = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 8 + 2 * C::NACC + i); };
   auto bar_vec_empty = [&](int i) { return bar0 + 8u * (2 * C::NSLOT + 10 + 2 * C::NACC + i); };
-  auto bar_xsc = [&](int set, int kt) {
-    return bar0 + 8u * (2 * C::NSLOT + 12 + 2 * C::NACC + 2 * set + kt);
-  };
-  auto bar_wfree = [&](int set) { return bar0 + 8u * (2 * C::NSLOT + 16 + 2 * C::NACC + set); };
+  auto bar_wfree = [&](int set) { return bar0 + 8u * (2 * C::NSLOT + 12 + 2 * C::NACC + set); };
   uint32_t* tmem_ptr_smem = reinterpret_cast<uint32_t*>(smem_raw + C::OFF_TMEMPTR);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -420,7 +418,6 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     }
     for (int set = 0; set < 2; ++set) {
       for (int w = 0; w < 4; ++w) mbar_init(bar_built(set, w), 8);  // 8 W warps of a k half
-      for (int kt = 0; kt < 2; ++kt) mbar_init(bar_xsc(set, kt), 4);  // one lane-quarter group
       mbar_init(bar_wfree(set), 1);  // MMA commit
     }
     for (int i = 0; i < C::NACC; ++i) {
@@ -536,11 +533,11 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
         if (elect_one()) mma_commit(bar_empty(slot(item)));
       };
       release(0), release(1), release(2);
-      // O2 += W[kt] . x~[kt] (W block wblk built, x~ scaled)
+      // O2 += W[kt] . x[kt] (W block wblk built in TMEM, x rows kt landed)
       const int set = lu & 1;
       const uint32_t upar = (lu >> 1) & 1;
-      auto gemm2 = [&](int wblk, int wa, int wb, int xi, int kt, bool first) {
-        mbar_wait(bar_xsc(set, kt), upar);
+      auto gemm2 = [&](int wblk, int wa, int wb, int xi, bool first) {
+        mbar_wait(bar_full(slot(xi)), par(xi));
         mbar_wait(bar_built(set, 2 * wblk), upar);
         mbar_wait(bar_built(set, 2 * wblk + 1), upar);
         tc_fence_after();
@@ -558,11 +555,11 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
                        (!first || kk > 0) ? 1u : 0u);
         }
       };
-      gemm2(0, 4, 5, 3, 0, true);
+      gemm2(0, 4, 5, 3, true);
       release(3);
       if (lane == 0 && lu < 20) SSD_TRACE(1400 + lu * 8 + 2);
       if (mt) {
-        gemm2(1, 7, 8, 6, 1, false);
+        gemm2(1, 7, 8, 6, false);
         release(6);
       }
       if (elect_one()) mma_commit(bar_wfree(set));  // this unit's W TMEM set read
@@ -576,8 +573,8 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     //   a_i  = dA_i log2 e
     //   xs_i = dt_i exp2(a_{k0(i)} - a_i), k0(i) = 16 floor(i / 16) (the MMA K step of i)
     // so that exp(dA_m - dA_k) dt_k = exp2(a_m - a_{k0(k)}) * xs_k: the first factor is
-    // one exp per (row, K step) applied to cb, the second a per-row scale of x (bounded:
-    // at most 16 positions of decay, <= 2^37 at the Mamba-2 initialisation ranges) ======
+    // one exp per (row, K step), the second a per-key multiplier (bounded: at most 16
+    // positions of decay), both applied to cb in fp32 before W is rounded ======
     int lu = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++lu) {
       int b, c, h, mt;
@@ -597,7 +594,8 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
     }
   } else if (warp >= C::W_WARP0 && warp < C::EPI_WARP0) {
     // ===== W builders: row r of a cb block, 32 keys per thread (key quarter kq):
-    //       W[m][k] = cb[m][k] exp2(a_m - a_{k0}) for k <= m and k < len, else 0 =====
+    //       W[m][k] = cb[m][k] exp2(a_m - a_{k0}) xs_k (= cb exp(dA_m - dA_k) dt_k) for k <= m
+    //       and k < len, else 0; one exp per row and K step, the x tile stays as loaded =====
     const int q4 = warp & 3;
     const int kq = (warp - C::W_WARP0) >> 2;  // key quarter of each 128-key block
     const int kh = kq >> 1;                   // the slot (64-key half) it lies in
@@ -611,40 +609,11 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
       mbar_wait(bar_vec_full(vb), (lu >> 1) & 1);
       const float* va = vec + vb * 2 * Q;
       const float* vxs = va + Q;
-      // x rows of k-tile kt: x~[k][p] = xs_k x[k][p] in place (row r = key r of the tile; a
-      // SW128 row stays a row, the walk starts at unit r & 7: no bank conflicts). k-tile 0 is
-      // scaled by key quarter 0 first, k-tile 1 (mt = 1 units) by key quarter 1 after its
-      // k-tile 0 W half.
-      auto scale_x = [&](int kt) {
-        const int item = kt ? 6 : 3;
-        const int s = (f + item) % C::NSLOT;
-        mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
-        const int k = kt * 128 + r;
-        const float w = k < len ? vxs[k] : 0.f;
-        const uint32_t row = sRing + s * SLOT + r * 128;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t addr = row + ((q ^ (r & 7)) << 4);
-          uint32_t v[4];
-          ld_shared_v4(addr, v);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 xf = unpack2<BF16>(v[e]);
-            v[e] = pack2rn<BF16>(xf.x * w, xf.y * w);
-          }
-          st_shared_v4(addr, v[0], v[1], v[2], v[3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_xsc(lu & 1, kt));
-      };
-      if (kq == 0) scale_x(0);
       // this unit's W TMEM set (lu & 1) was read by the MMAs of unit lu - 2
       if (lu >= 2) mbar_wait(bar_wfree(lu & 1), ((lu >> 1) - 1) & 1);
       tc_fence_after();
       const int nblk = mt ? 2 : 1;
       for (int bi = 0; bi < nblk; ++bi) {  // bi = k-tile of the block
-        if (bi == 1 && kq == 1) scale_x(1);
         const int item = bi ? 7 + kh : 4 + kh;
         const int s = (f + item) % C::NSLOT;
         mbar_wait(bar_full(s), ((f + item) / C::NSLOT) & 1);
@@ -656,7 +625,7 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {  // the thread's two K steps (16 keys each)
           const int k0 = bi * 128 + 32 * kq + 16 * ks;
-          // W[m][k] = cb[m][k] exp2(a_m - a_{k0}) for k <= m, k < len (x carries xs_k)
+          // W[m][k] = cb[m][k] exp2(a_m - a_{k0}) xs_k for k <= m, k < len
           const float sc = (k0 <= m && k0 < len) ? ex2(am - va[k0]) : 0.f;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -667,11 +636,15 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (kb <= m && kb < len) {  // else the whole unit is masked
               ld_shared_v4(addr, v);
+              // xs of the 8 keys (the same for every row: broadcast reads)
+              const float4 xa = *reinterpret_cast<const float4*>(vxs + kb);
+              const float4 xb = *reinterpret_cast<const float4*>(vxs + kb + 4);
+              const float xk[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
               const bool edge = kb + 7 > m || kb + 7 >= len;  // the diagonal / last unit
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 cbv = unpack2<BF16>(v[e]);
-                float w0 = cbv.x * sc, w1 = cbv.y * sc;
+                float w0 = cbv.x * sc * xk[2 * e], w1 = cbv.y * sc * xk[2 * e + 1];
                 if (edge) {
                   const int k = kb + 2 * e;
                   if (k > m || k >= len) w0 = 0.f;
