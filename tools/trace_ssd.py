@@ -28,8 +28,14 @@ torch.cuda.synchronize()
 tr = buf.cpu().tolist()
 t0 = min(v for v in tr if v)
 f = lambda v: f"{v - t0:7d}" if v else "      -"  # noqa: E731
-for lu in range(6):
-    print(f"unit {lu}: items issued", " ".join(f(tr[lu * 13 + i]) for i in range(13)))
-    print("   W blocks loaded/built", " ".join(f(tr[1000 + lu * 12 + j]) for j in range(12)))
-    print("   MMA start g1a g1b g2a g2b g2c", " ".join(f(tr[1400 + lu * 8 + j]) for j in range(6)))
+# CTA 0 owns units 0, G, 2G, ... (G = the odd persistent grid): mt alternates 0, 1, 0, ...
+f0 = 0
+for lu in range(8):
+    mt = lu & 1
+    ni = 9 if mt else 6
+    print(f"unit {lu} (mt {mt}): items issued", " ".join(f(tr[f0 + i]) for i in range(ni)))
+    f0 += ni
+    print("   W block0 k-half0 loaded/built, k-half1 loaded/built; block1 ...",
+          " ".join(f(tr[1000 + lu * 12 + j]) for j in range(4 + 4 * mt)))
+    print("   MMA start / after C.prev / after W0.x / end", " ".join(f(tr[1400 + lu * 8 + j]) for j in range(4)))
     print("   epi", f(tr[1600 + lu * 2]), f(tr[1601 + lu * 2]))
