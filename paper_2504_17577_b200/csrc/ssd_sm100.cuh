@@ -636,15 +636,19 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (kb <= m && kb < len) {  // else the whole unit is masked
               ld_shared_v4(addr, v);
-              // xs of the 8 keys (the same for every row: broadcast reads)
+              // per-key factors sc * xs_k of the 8 keys (xs: the same for every row, broadcast
+              // reads), then one paired multiply per key pair
               const float4 xa = *reinterpret_cast<const float4*>(vxs + kb);
               const float4 xb = *reinterpret_cast<const float4*>(vxs + kb + 4);
-              const float xk[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+              const uint64_t sc2 = f2pack(sc, sc);
+              const uint64_t fk[4] = {fmul2(f2pack(xa.x, xa.y), sc2), fmul2(f2pack(xa.z, xa.w), sc2),
+                                      fmul2(f2pack(xb.x, xb.y), sc2), fmul2(f2pack(xb.z, xb.w), sc2)};
               const bool edge = kb + 7 > m || kb + 7 >= len;  // the diagonal / last unit
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 cbv = unpack2<BF16>(v[e]);
-                float w0 = cbv.x * sc * xk[2 * e], w1 = cbv.y * sc * xk[2 * e + 1];
+                float w0, w1;
+                f2unpack(fmul2(f2pack(cbv.x, cbv.y), fk[e]), w0, w1);
                 if (edge) {
                   const int k = kb + 2 * e;
                   if (k > m || k >= len) w0 = 0.f;
