@@ -96,6 +96,14 @@ __device__ __forceinline__ uint32_t pack2rn(float lo, float hi) {
   else asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// packed 16-bit multiply (RN), two lanes per 32-bit register
+template <bool BF16>
+__device__ __forceinline__ uint32_t hmul2rn(uint32_t a, uint32_t b) {
+  uint32_t r;
+  if constexpr (BF16) asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  else asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
 __device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -636,8 +644,10 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (kb <= m && kb < len) {  // else the whole unit is masked
               ld_shared_v4(addr, v);
-              // per-key factors sc * xs_k of the 8 keys (xs: the same for every row, broadcast
-              // reads), then one paired multiply per key pair
+              // per-key factors sc * xs_k of the 8 keys in fp32 (xs: the same for every row,
+              // broadcast reads; the product is exp(dA_m - dA_k) dt_k <= dt_k for k <= m),
+              // rounded to the 16-bit type, then one packed 16-bit multiply per key pair:
+              // W = RN(cb RN(sc xs_k)) (masked keys: bits cleared after the multiply)
               const float4 xa = *reinterpret_cast<const float4*>(vxs + kb);
               const float4 xb = *reinterpret_cast<const float4*>(vxs + kb + 4);
               const uint64_t sc2 = f2pack(sc, sc);
@@ -646,15 +656,15 @@ tl_ssd_scan_kernel(const __grid_constant__ SsdParams p) {
               const bool edge = kb + 7 > m || kb + 7 >= len;  // the diagonal / last unit
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 cbv = unpack2<BF16>(v[e]);
-                float w0, w1;
-                f2unpack(fmul2(f2pack(cbv.x, cbv.y), fk[e]), w0, w1);
+                float f0, f1;
+                f2unpack(fk[e], f0, f1);
+                uint32_t w = hmul2rn<BF16>(v[e], pack2rn<BF16>(f0, f1));
                 if (edge) {
                   const int k = kb + 2 * e;
-                  if (k > m || k >= len) w0 = 0.f;
-                  if (k + 1 > m || k + 1 >= len) w1 = 0.f;
+                  if (k > m || k >= len) w &= 0xffff0000u;
+                  if (k + 1 > m || k + 1 >= len) w &= 0x0000ffffu;
                 }
-                v[e] = pack2rn<BF16>(w0, w1);
+                v[e] = w;
               }
             }
 #pragma unroll
