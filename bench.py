@@ -513,6 +513,7 @@ def bench_one(cfg, pk, steps=20, warmup=3, graph=False):
         floor_ms = n_exp / (n_sm * 16 * mhz * 1e6) * 1e3
         res.update({"mufu_floor_ms": floor_ms, "frac_of_mufu_floor": floor_ms / kern_ms,
                     "mufu_floor_clock_mhz": mhz})
+    res["clocks"] = {k: ck.get(k) for k in ("sm_mhz", "reasons")}
     if small:
         res["note"] = "L2 flushed between launches (256 MB write)"
     if graph:
