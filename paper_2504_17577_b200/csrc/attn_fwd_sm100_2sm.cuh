@@ -16,6 +16,14 @@
 //   commits are multicast to both CTAs' barriers. Each CTA runs its own producer and two
 //   softmax warpgroups on its own rows; their S-read / P-written signals arrive on the
 //   leader's barriers (remote mbarrier arrive, cluster scope).
+//
+//   The two query tiles of a unit run in two independent "slots" (slot t = TMEM S_t / O_t,
+//   smem Q_t / P_t, issuer warp 1+t, softmax warpgroup t). Each slot's Q tile is loaded
+//   (both halves, by the peer's warp 1+t) as soon as its previous tile's last QK^T has completed, and the key blocks only the longer tile of a causal unit
+//   needs are released by that tile's issuer alone (two commits on the ring slot's "empty"
+//   barrier). So the slot that finishes a unit first starts the next unit while the other
+//   slot still works through its extra blocks, instead of idling until both are done;
+//   the longer tile of the next unit goes to the slot that is ahead (slot_assign).
 #pragma once
 #include "attn_fwd_sm100.cuh"
 
@@ -87,6 +95,36 @@ __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
   return U;
 }
 
+// Which query tile of unit U slot t runs (tau = 0 / 1, or -1: none), its block count n and
+// the other slot's block count n_oth (blocks j >= n_oth are this slot's alone). p0 / p1
+// count the blocks each slot has been given so far (every role keeps its own copy and
+// updates it identically): the slot that is ahead (fewer blocks so far, so it finishes its
+// current tile first) gets the longer tile, so both slots tend to finish the unit together
+// and a slot's extra causal blocks overlap the other slot's next tile. Ties give the longer
+// tile to slot 1; a one-tile unit (short-sequence mode) goes to the slot that is ahead.
+struct SlotAsg {
+  int tau, n, n_oth;
+};
+__device__ __forceinline__ SlotAsg slot_assign(const Unit2& U, int t, int& p0, int& p1) {
+  SlotAsg a;
+  if (U.tiles == 1) {
+    const int s = (p1 < p0) ? 1 : 0;
+    a.tau = (t == s) ? 0 : -1;
+    a.n = (t == s) ? U.n0 : 0;
+    a.n_oth = (t == s) ? 0 : U.n0;
+    if (s == 0) p0 += U.n0; else p1 += U.n0;
+  } else {
+    const int ls = (p0 < p1) ? 0 : 1;
+    const int tl = (U.n1 >= U.n0) ? 1 : 0;
+    const int nl = max(U.n0, U.n1), ns = min(U.n0, U.n1);
+    a.tau = (t == ls) ? tl : 1 - tl;
+    a.n = (t == ls) ? nl : ns;
+    a.n_oth = (t == ls) ? ns : nl;
+    if (ls == 0) { p0 += nl; p1 += ns; } else { p1 += nl; p0 += ns; }
+  }
+  return a;
+}
+
 template <bool BF16, class PT = AttnParams>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
@@ -104,8 +142,9 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
   const uint32_t sP = base + C::OFF_P;
   const uint32_t sSched = base + C::OFF_SCHED;
   const uint32_t bar0 = base + C::OFF_BAR;
-  const uint32_t bar_q_full = bar0;
-  const uint32_t bar_q_empty = bar0 + 8u;
+  // per-slot Q barriers: slot 0 at indices 0 / 1, slot 1 at the end of the block
+  auto bar_q_full = [&](int t) { return t == 0 ? bar0 : bar0 + 8u * (2 + 2 * C::NST + 18); };
+  auto bar_q_empty = [&](int t) { return t == 0 ? bar0 + 8u : bar0 + 8u * (2 + 2 * C::NST + 19); };
   auto bar_kv_full = [&](int s) { return bar0 + 8u * (2 + s); };
   auto bar_kv_empty = [&](int s) { return bar0 + 8u * (2 + C::NST + s); };
   auto bar_s_full = [&](int t) { return bar0 + 8u * (2 + 2 * C::NST + t); };
@@ -126,8 +165,10 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
     prefetch_tmap(&p.tm_q);
     prefetch_tmap(&p.tm_k);
     prefetch_tmap(&p.tm_v);
-    mbar_init(bar_q_full, 1);
-    mbar_init(bar_q_empty, 2);
+    for (int t = 0; t < TILES; ++t) {
+      mbar_init(bar_q_full(t), 1);   // the leader issuer's expect_tx (+ both halves' bytes)
+      mbar_init(bar_q_empty(t), 1);  // commit after the tile's last QK^T
+    }
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(bar_kv_full(s), 1);
       mbar_init(bar_kv_empty(s), 2);
@@ -141,7 +182,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_sched_full(i), 1);
-      mbar_init(bar_sched_empty(i), 2 + 8 + 8 + 1);  // issuers, softmax warps x2, peer producer
+      mbar_init(bar_sched_empty(i), 2 + 8 + 8 + 1 + 2);  // issuers, softmax warps x2, peer producer, peer Q loaders
     }
     fence_mbar_init();
   }
@@ -156,11 +197,9 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
     if (warp == 0) {
       // =========================== TMA producer (both CTAs) + CLC (leader) =================
       if (lane == 0) {
-        const uint64_t pol_q = policy_evict_first();
         const uint64_t pol_kv = policy_evict_last();
         int unit = blockIdx.x >> 1;
         int it = 0;
-        const uint32_t lead_q_full = mapa_shared(bar_q_full, 0);
         for (int k = 0;; ++k) {
           const int sl = k & 1;
           mbar_arrive_expect_tx(bar_sched_full(sl), 16);
@@ -170,24 +209,8 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
           }
           const Unit2 U = decode_unit2(unit, p);
           const int nmax = max(U.n0, U.n1);
-          if (k >= 1) mbar_wait(bar_q_empty, (k - 1) & 1);
-          if (leader) {
-            uint32_t qbytes = 0;
-            for (int t = 0; t < U.tiles; ++t)
-              for (int c = 0; c < 2; ++c)
-                if (U.r0 + 256 * t + 128 * c < p.Sq) qbytes += C::Q_TILE_BYTES;
-            mbar_arrive_expect_tx(bar_q_full, qbytes);
-          }
-#pragma unroll
-          for (int t = 0; t < TILES; ++t) {
-            const int rq = U.r0 + 256 * t + 128 * (int)rank;
-            if (t < U.tiles && rq < p.Sq) {
-#pragma unroll
-              for (int c = 0; c < D / 64; ++c)
-                tma_load_4d_2sm(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, lead_q_full,
-                                c * 64, U.h, rq, U.b, pol_q);
-            }
-          }
+          // (Q tiles are loaded per slot: leader half by the slot's issuer, peer half by the
+          // peer's warp 1+t, each as soon as the slot's previous tile no longer reads it)
           // ring order = MMA consumption order: K_0, K_1, V_0, K_2, V_1, ..., V_{nmax-1}
           for (int q = 0; q < 2 * nmax; ++q, ++it) {
             const bool is_k = (q == 0) || ((q & 1) && q != 2 * nmax - 1);
@@ -232,16 +255,19 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
         const uint32_t pa = sP + t * C::P_TILE_BYTES;
         int unit = blockIdx.x >> 1;
         int it = 0;
-        uint32_t cs = 0, cpv = 0;
+        int p0 = 0, p1 = 0;
+        uint32_t cs = 0, cpv = 0, cq = 0;
         for (int k = 0;; ++k) {
           const Unit2 U = decode_unit2(unit, p);
+          const SlotAsg A = slot_assign(U, t, p0, p1);
           const int nmax = max(U.n0, U.n1);
-          const int nt = t ? U.n1 : U.n0;
+          const int nt = A.n;
+          if (lane == 0) TL_TRACE2(k, 6000 + 100 * t + 2);  // unit decoded
           const int it0 = it;
           it += 2 * nmax;
           auto kpos = [&](int j) { return it0 + (j == 0 ? 0 : 2 * j - 1); };
           auto vpos = [&](int j) { return it0 + (j == nmax - 1 ? 2 * nmax - 1 : 2 * j + 2); };
-          mbar_wait(bar_q_full, k & 1);
+          if (nt > 0) mbar_wait(bar_q_full(t), cq & 1);  // Q_t (loaded by the peer's warp 1+t)
           if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 7);  // Q ready (unit start)
           auto issue_s = [&](int j) {
             const int sl = kpos(j) % C::NST;
@@ -263,6 +289,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             }
             if (elect_one()) mma_commit_2sm(bar_s_full(t));
             if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
+            if (j >= A.n_oth && elect_one()) mma_commit_2sm(bar_kv_empty(sl));  // this slot's alone
             ++cs;
           };
           auto issue_pv = [&](int j) {
@@ -291,33 +318,69 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             }
             if (elect_one()) mma_commit_2sm(bar_o_done(t));
             if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
+            if (j >= A.n_oth && elect_one()) mma_commit_2sm(bar_kv_empty(sl));  // this slot's alone
             ++cpv;
           };
           if (nt > 0) {
             issue_s(0);
-            if (nt == 1 && elect_one()) mma_commit_2sm(bar_q_empty);
+            if (nt == 1 && elect_one()) mma_commit_2sm(bar_q_empty(t));
             for (int j = 0; j < nt; ++j) {
               if (j + 1 < nt) {
                 issue_s(j + 1);
-                if (j + 2 == nt && elect_one()) mma_commit_2sm(bar_q_empty);
+                if (j + 2 == nt && elect_one()) mma_commit_2sm(bar_q_empty(t));
               }
               issue_pv(j);
             }
-          } else {
-            if (elect_one()) mma_commit_2sm(bar_q_empty);
+            ++cq;
           }
-          for (int j = nt; j < nmax; ++j) {  // blocks only the other tile needs
-            int sl = kpos(j) % C::NST;
-            mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
-            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
-            sl = vpos(j) % C::NST;
-            mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
-            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
-          }
+          // (blocks j >= nt belong to the other slot alone, which releases them itself)
           if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 6);  // issuer done with the unit's MMAs
           mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+          if (lane == 0) TL_TRACE2(k, 6000 + 100 * t + 0);  // next unit's CLC response seen
           const int nxt = clc_query(sSched + 16 * (k & 1));
           if (elect_one()) mbar_arrive(bar_sched_empty(k & 1));
+          if (lane == 0) TL_TRACE2(k, 6000 + 100 * t + 1);
+          if (nxt < 0) break;
+          unit = nxt >> 1;
+        }
+      }
+      __syncwarp();
+    } else if ((warp == 1 || warp == 2) && !leader) {
+      // ===== Q loaders (peer warps 1, 2: slot t = warp - 1): both halves of each of the
+      // slot's Q tiles, issued as soon as the slot's previous tile's last QK^T has completed
+      // (q_empty, multicast commit: the peer's own copy): the peer's rows with a 2-SM load,
+      // the leader's rows multicast into the leader's smem; the expected bytes are posted on
+      // the leader's q_full by a remote arrive. The leader's issuer only waits q_full. =====
+      const int t = warp - 1;
+      if (lane == 0) {
+        const uint64_t pol_q = policy_evict_first();
+        const uint32_t lead_q_full = mapa_shared(bar_q_full(t), 0);
+        int unit = blockIdx.x >> 1;
+        int p0 = 0, p1 = 0;
+        uint32_t cq = 0;
+        for (int k = 0;; ++k) {
+          const Unit2 U = decode_unit2(unit, p);
+          const SlotAsg A = slot_assign(U, t, p0, p1);
+          if (A.n > 0) {
+            if (cq > 0) mbar_wait(bar_q_empty(t), (cq - 1) & 1);
+            const int r = U.r0 + 256 * A.tau;
+            const bool two = r + 128 < p.Sq;
+            mbar_arrive_expect_tx_cluster(lead_q_full, (two ? 2 : 1) * C::Q_TILE_BYTES);
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c)  // leader's rows [r, r + 128)
+              tma_load_4d_mc(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, bar_q_full(t),
+                             c * 64, U.h, r, U.b, (uint16_t)1, pol_q);
+            if (two) {
+#pragma unroll
+              for (int c = 0; c < D / 64; ++c)  // own rows [r + 128, r + 256)
+                tma_load_4d_2sm(sQ + t * C::Q_TILE_BYTES + c * CHUNK_BYTES, &p.tm_q, lead_q_full,
+                                c * 64, U.h, r + 128, U.b, pol_q);
+            }
+            ++cq;
+          }
+          mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
+          const int nxt = clc_query(sSched + 16 * (k & 1));
+          mbar_arrive_cluster(mapa_shared(bar_sched_empty(k & 1), 0));
           if (nxt < 0) break;
           unit = nxt >> 1;
         }
@@ -342,14 +405,16 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
     const float c = p.c_log2;
     int unit = blockIdx.x >> 1;
     uint32_t g = 0;
+    int p0 = 0, p1 = 0;
     for (int k = 0;; ++k) {
       const Unit2 U = decode_unit2(unit, p);
+      const SlotAsg A = slot_assign(U, t, p0, p1);
 #ifdef TLATTN_MMA_ONLY
       const int nt = 0;
 #else
-      const int nt = t ? U.n1 : U.n0;
+      const int nt = A.n;
 #endif
-      if (t >= U.tiles) {  // short-sequence mode: this warpgroup's tile is not in the unit
+      if (A.tau < 0) {  // short-sequence mode: the unit's one tile runs in the other slot
         mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
         const int nxt = clc_query(sSched + 16 * (k & 1));
         __syncwarp();
@@ -358,7 +423,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
         unit = nxt >> 1;
         continue;
       }
-      const int row = U.r0 + 256 * t + 128 * (int)rank + lr;
+      const int row = U.r0 + 256 * A.tau + 128 * (int)rank + lr;
       const int limit = p.causal ? min(p.Skv - 1, row + p.Skv - p.Sq) : (p.Skv - 1);
       float m = -INFINITY;
       float l = 0.f;
@@ -486,6 +551,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
         mbar_wait(bar_o_done(t), (g - 1) & 1);
         tc_fence_after();
       }
+      if (lane == 0 && q4 == 0) TL_TRACE2(k, 6500 + 100 * t + 0);  // epilogue start (last PV done)
       const float inv_l = (l > 0.f) ? (1.f / l) : 0.f;
       const bool row_ok = row < p.Sq;
       if (nt == 0) {  // no PV this unit: P_t may still feed the previous unit's O store
@@ -518,8 +584,9 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
       }
       fence_proxy_async_smem();
       named_bar_sync(1 + t, 128);
+      if (lane == 0 && q4 == 0) TL_TRACE2(k, 6500 + 100 * t + 1);  // O tile staged
       if (lr == 0) {
-        const int row0 = U.r0 + 256 * t + 128 * (int)rank;
+        const int row0 = U.r0 + 256 * A.tau + 128 * (int)rank;
         if (row0 < p.Sq) {
 #pragma unroll
           for (int c2 = 0; c2 < D / 64; ++c2) {
@@ -539,10 +606,12 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
       if (row_ok)
         store_lse(p, U.b, U.h, row, (l > 0.f) ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY);
       tc_fence_before();
+      if (lane == 0 && q4 == 0) TL_TRACE2(k, 6500 + 100 * t + 2);  // LSE stored
       mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
       const int nxt = clc_query(sSched + 16 * (k & 1));
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_sched_empty(k & 1), 0));
+      if (lane == 0 && q4 == 0) TL_TRACE2(k, 6500 + 100 * t + 3);  // next unit known
       if (nxt < 0) break;
       unit = nxt >> 1;
     }
