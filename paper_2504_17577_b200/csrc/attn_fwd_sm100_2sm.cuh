@@ -290,6 +290,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             if (elect_one()) mma_commit_2sm(bar_s_full(t));
             if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
             if (j >= A.n_oth && elect_one()) mma_commit_2sm(bar_kv_empty(sl));  // this slot's alone
+            if (lane == 0 && j < 15) TL_TRACE2(k, 4000 + 1000 * t + 8 * j + 6);  // S(j) issued (after commit)
             ++cs;
           };
           auto issue_pv = [&](int j) {
@@ -319,6 +320,7 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             if (elect_one()) mma_commit_2sm(bar_o_done(t));
             if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
             if (j >= A.n_oth && elect_one()) mma_commit_2sm(bar_kv_empty(sl));  // this slot's alone
+            if (lane == 0 && j < 15) TL_TRACE2(k, 4000 + 1000 * t + 8 * j + 7);  // PV(j) issued (after commit)
             ++cpv;
           };
           if (nt > 0) {
