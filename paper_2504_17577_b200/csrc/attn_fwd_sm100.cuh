@@ -545,6 +545,8 @@ tl_attn_fwd_kernel(const __grid_constant__ PT p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_smem;
+  griddep_wait();  // PDL (see attn_fwd_sm100_2sm.cuh)
+  if (threadIdx.x == 0) griddep_launch_dependents();
 
   // Register rebalancing: warpgroup 0 (load / MMA / spare warps) gives registers to the
   // two softmax warpgroups, which hold a 128-column fp32 S row per thread.

@@ -191,6 +191,10 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive / 2-SM TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_smem;
+  // PDL: everything above (barrier init, TMEM allocation, tensor-map prefetch) may overlap
+  // the previous grid's tail; global memory is touched only after this
+  griddep_wait();
+  if (threadIdx.x == 0) griddep_launch_dependents();
 
   if (warp < 4) {
     setmaxnreg_dec<REGS_SMALL>();

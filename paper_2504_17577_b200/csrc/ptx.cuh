@@ -424,6 +424,14 @@ __device__ __forceinline__ void mma_f16_ts_2sm(uint32_t tmem_d, uint32_t tmem_a,
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Programmatic dependent launch (the kernel is launched with programmatic stream
+// serialization): wait until the previous grid in the stream has completed and its memory
+// is visible (every thread that touches global memory passes this first), and let the next
+// grid begin launching (its prologue overlaps this grid's tail). No-ops without PDL.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 // commit: arrive once on `bar` (same smem offset) in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_2sm(uint32_t bar) {
   asm volatile(

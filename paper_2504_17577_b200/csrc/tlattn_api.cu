@@ -189,6 +189,27 @@ bool encode_bshd(PFN_cuTensorMapEncodeTiled_v12000 enc, CUtensorMap* m, const vo
                           {64, 1, box_rows, 1});
 }
 
+// Kernel launch with programmatic dependent launch allowed (the kernels call
+// griddep_wait() before touching global memory): back-to-back calls overlap the next
+// kernel's launch and prologue with this one's tail. -DTLATTN_NO_PDL: plain launches.
+template <class K, class PT>
+cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       const PT& prm) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+#ifndef TLATTN_NO_PDL
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+#endif
+  return cudaLaunchKernelEx(&cfg, kern, prm);
+}
+
 template <bool BF16, class PT>
 int launch_2sm(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
   auto kern = tl_attn_fwd_kernel_2sm<BF16, PT>;
@@ -203,8 +224,10 @@ int launch_2sm(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
       di.smem_set[inst] = true;
     }
   }
-  kern<<<2 * prm.n_units, NUM_THREADS, KCfg2::SMEM_BYTES, stream>>>(prm);
-  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  if (launch_pdl(kern, 2 * prm.n_units, NUM_THREADS, KCfg2::SMEM_BYTES, stream, prm) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
   return TL_OK;
 }
 
@@ -226,8 +249,10 @@ int launch(const PT& prm, DeviceInfo& di, int inst, cudaStream_t stream) {
       di.smem_set[inst] = true;
     }
   }
-  kern<<<prm.n_units, NUM_THREADS, KCfg<D>::SMEM_BYTES, stream>>>(prm);
-  if (cudaGetLastError() != cudaSuccess) return TL_ERR_CUDA;
+  if (launch_pdl(kern, prm.n_units, NUM_THREADS, KCfg<D>::SMEM_BYTES, stream, prm) != cudaSuccess) {
+    cudaGetLastError();
+    return TL_ERR_CUDA;
+  }
   return TL_OK;
 }
 
