@@ -473,6 +473,17 @@ def ncu_traffic(name, world):
         return None
 
 
+# The `also` block times every config from the same starting state: 0.3 s of idle GPU after
+# its inputs are generated (input generation and the previous config heat the chip into its
+# power limit, which otherwise lands on whichever config comes next).
+ALSO_IDLE_S = 0.3
+
+
+def settle():
+    torch.cuda.synchronize()
+    time.sleep(ALSO_IDLE_S)
+
+
 def bench_one(cfg, pk, steps=20, warmup=3, graph=False):
     from paper_2504_17577_b200 import attention
     from paper_2504_17577_b200.inputs import gen_qkv
@@ -485,6 +496,7 @@ def bench_one(cfg, pk, steps=20, warmup=3, graph=False):
     def call():
         attention(q, k, v, causal=cfg.causal, scale=cfg.scale, out=o, lse_out=lse)
 
+    settle()
     for _ in range(warmup):
         call()
     st = torch.cuda.current_stream()
@@ -514,6 +526,7 @@ def bench_one(cfg, pk, steps=20, warmup=3, graph=False):
         res.update({"mufu_floor_ms": floor_ms, "frac_of_mufu_floor": floor_ms / kern_ms,
                     "mufu_floor_clock_mhz": mhz})
     res["clocks"] = {k: ck.get(k) for k in ("sm_mhz", "reasons")}
+    res["idle_before_s"] = ALSO_IDLE_S
     if small:
         res["note"] = "L2 flushed between launches (256 MB write)"
     if graph:
@@ -564,6 +577,7 @@ def bench_mla(cfg, pk, steps=20, warmup=3):
     def call():
         mla_decode(q, qp, kv, kp, seqlens=sld, out=o, lse_out=lse, workspace=ws)
 
+    settle()
     for _ in range(warmup):
         call()
     st = torch.cuda.current_stream()
@@ -607,6 +621,7 @@ def bench_ssd(cfg, pk, steps=10, warmup=3):
 
         def call():
             ssd_chunk_scan(cb, x, dt, dA, C, prev, D, out=out)
+    settle()
     for _ in range(warmup):
         call()
     st = torch.cuda.current_stream()
@@ -642,6 +657,7 @@ def bench_gemm(name, pk, iters=10):
     c = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
 
     def med(fn):
+        settle()
         for _ in range(3):
             fn()
         evs = []
