@@ -101,14 +101,18 @@ __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
 // updates it identically): the slot that is ahead (fewer blocks so far, so it finishes its
 // current tile first) gets the longer tile, so both slots tend to finish the unit together
 // and a slot's extra causal blocks overlap the other slot's next tile. Ties give the longer
-// tile to slot 1; a one-tile unit (short-sequence mode) goes to the slot that is ahead.
+// tile to slot 1. One-tile units (short-sequence mode) always run in slot 0: a slot may run
+// ahead of the other only by the <= 4 ring items of a causal unit's extra blocks (fewer than
+// the NST = 6 ring slots, so a waiter is never two phases ahead of a slot's "full" barrier);
+// one-tile units alternating between slots would let a slot jump a whole unit of items ahead
+// and read a "full" phase of the previous revolution (parity aliasing: measured hang).
 struct SlotAsg {
   int tau, n, n_oth;
 };
 __device__ __forceinline__ SlotAsg slot_assign(const Unit2& U, int t, int& p0, int& p1) {
   SlotAsg a;
   if (U.tiles == 1) {
-    const int s = (p1 < p0) ? 1 : 0;
+    const int s = 0;
     a.tau = (t == s) ? 0 : -1;
     a.n = (t == s) ? U.n0 : 0;
     a.n_oth = (t == s) ? 0 : U.n0;

@@ -51,6 +51,11 @@ def test_parity_small(B, Hq, Hkv, Sq, Skv, D, dtype, causal):
     (2, 4, 2, 300, 300, True),       # ragged, GQA
     (1, 3, 1, 700, 900, True),       # Sq < Skv, ragged, odd unit count
     (1, 2, 2, 900, 600, False),      # Sq > Skv
+    # several units per CTA pair, so both slots of the pair run tiles (the one-tile units
+    # of the short-sequence mode go to the slot that is ahead; causal 512-row units give
+    # the longer tile to it, slot_assign)
+    (4, 32, 8, 512, 512, True),
+    (2, 16, 16, 768, 640, False),
 ])
 @pytest.mark.parametrize("tiles", ["1", "2"])
 def test_pair_kernel_unit_modes(B, Hq, Hkv, Sq, Skv, causal, tiles):
