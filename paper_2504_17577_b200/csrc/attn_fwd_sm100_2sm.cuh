@@ -19,11 +19,13 @@
 //
 //   The two query tiles of a unit run in two independent "slots" (slot t = TMEM S_t / O_t,
 //   smem Q_t / P_t, issuer warp 1+t, softmax warpgroup t). Each slot's Q tile is loaded
-//   (both halves, by the peer's warp 1+t) as soon as its previous tile's last QK^T has completed, and the key blocks only the longer tile of a causal unit
-//   needs are released by that tile's issuer alone (two commits on the ring slot's "empty"
+//   (both halves, by the peer's warp 1+t) as soon as its previous tile's last QK^T has
+//   completed, and the (at most 2) key blocks only the longer tile of a causal unit needs
+//   are released by that tile's issuer alone (two commits on the ring slot's "empty"
 //   barrier). So the slot that finishes a unit first starts the next unit while the other
 //   slot still works through its extra blocks, instead of idling until both are done;
-//   the longer tile of the next unit goes to the slot that is ahead (slot_assign).
+//   the longer tile of the next unit goes to the slot that is ahead (slot_assign). When the
+//   tiles differ by more (a tile past the end of Sq) the slots walk the ring in step.
 #pragma once
 #include "attn_fwd_sm100.cuh"
 
@@ -106,24 +108,31 @@ __device__ __forceinline__ Unit2 decode_unit2(int u, const AttnParams& p) {
 // the NST = 6 ring slots, so a waiter is never two phases ahead of a slot's "full" barrier);
 // one-tile units alternating between slots would let a slot jump a whole unit of items ahead
 // and read a "full" phase of the previous revolution (parity aliasing: measured hang).
+// n_skip: blocks [n, n_skip) this slot's issuer still waits for and releases (one commit
+// each, the other slot's issuer commits once too): set when the other tile is longer by
+// more than 2 blocks (a tile past the end of Sq), where skipping them would let this slot
+// jump more than the 4-item bound ahead (see above); otherwise n_skip = n and the longer
+// tile's issuer releases its extra blocks alone (j >= n_oth: two commits).
 struct SlotAsg {
-  int tau, n, n_oth;
+  int tau, n, n_oth, n_skip;
 };
 __device__ __forceinline__ SlotAsg slot_assign(const Unit2& U, int t, int& p0, int& p1) {
   SlotAsg a;
   if (U.tiles == 1) {
-    const int s = 0;
-    a.tau = (t == s) ? 0 : -1;
-    a.n = (t == s) ? U.n0 : 0;
-    a.n_oth = (t == s) ? 0 : U.n0;
-    if (s == 0) p0 += U.n0; else p1 += U.n0;
+    a.tau = (t == 0) ? 0 : -1;
+    a.n = (t == 0) ? U.n0 : 0;
+    a.n_oth = (t == 0) ? 0 : U.n0;
+    a.n_skip = a.n;
+    p0 += U.n0;
   } else {
     const int ls = (p0 < p1) ? 0 : 1;
     const int tl = (U.n1 >= U.n0) ? 1 : 0;
     const int nl = max(U.n0, U.n1), ns = min(U.n0, U.n1);
+    const bool lock = nl - ns > 2;
     a.tau = (t == ls) ? tl : 1 - tl;
     a.n = (t == ls) ? nl : ns;
-    a.n_oth = (t == ls) ? ns : nl;
+    a.n_oth = (t == ls) ? (lock ? nl : ns) : nl;
+    a.n_skip = (t == ls || !lock) ? a.n : nl;
     if (ls == 0) { p0 += nl; p1 += ns; } else { p1 += nl; p0 += ns; }
   }
   return a;
@@ -343,7 +352,16 @@ tl_attn_fwd_kernel_2sm(const __grid_constant__ PT p) {
             }
             ++cq;
           }
-          // (blocks j >= nt belong to the other slot alone, which releases them itself)
+          // blocks j >= nt belong to the other slot; it releases them alone unless the other
+          // tile is much longer (n_skip > nt): then this slot walks them in step
+          for (int j = nt; j < A.n_skip; ++j) {
+            int sl = kpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (kpos(j) / C::NST) & 1);
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
+            sl = vpos(j) % C::NST;
+            mbar_wait(bar_kv_full(sl), (vpos(j) / C::NST) & 1);
+            if (elect_one()) mma_commit_2sm(bar_kv_empty(sl));
+          }
           if (lane == 0) TL_TRACE2(k, 4000 + 1000 * t + 8 * 15 + 6);  // issuer done with the unit's MMAs
           mbar_wait(bar_sched_full(k & 1), (k >> 1) & 1);
           if (lane == 0) TL_TRACE2(k, 6000 + 100 * t + 0);  // next unit's CLC response seen

@@ -314,3 +314,34 @@ def test_parity_fuzz(case):
     B, Hq, Hkv, Sq, Skv, D, dtype, causal = case
     q, k, v = gen(B, Hq, Hkv, Sq, Skv, D, dtype, 9000 + Sq * 7 + Skv)
     check_against_oracle(q, k, v, causal, default_scale(D), label=str(case))
+
+
+def _fuzz_many_units(n=12, seed=4017):
+    """Shapes with several 512-row units per CTA pair (so both tile slots of a pair move
+    through many units, the longer causal tile alternating between them) and ragged or
+    offset causal geometry (Sq != Skv: units whose first tile sees no key at all)."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        Hkv = int(rng.choice([2, 4, 8]))
+        Hq = Hkv * int(rng.choice([1, 2, 4]))
+        B = int(rng.integers(2, 9))
+        Sq = int(rng.integers(300, 2600))
+        Skv = Sq if rng.random() < 0.5 else int(rng.integers(200, 2600))
+        causal = bool(rng.random() < 0.7)
+        cases.append((B, Hq, Hkv, Sq, Skv, causal))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_many_units(), ids=lambda c: "B{}H{}/{}S{}x{}{}".format(
+    c[0], c[1], c[2], c[3], c[4], "c" if c[5] else ""))
+def test_parity_fuzz_many_units(case):
+    """CTA-pair kernel (D = 128) with many units per pair: sampled rows of every head (the
+    first 64, every unit / tile boundary, the last 16) against the oracle."""
+    B, Hq, Hkv, Sq, Skv, causal = case
+    q, k, v = gen(B, Hq, Hkv, Sq, Skv, 128, BF, 7000 + Sq * 3 + Skv)
+    rows = sorted(set(list(range(min(64, Sq))) +
+                      [r for t in range(0, Sq, 128) for r in (t, t + 127) if r < Sq] +
+                      list(range(max(0, Sq - 16), Sq))))
+    check_against_oracle(q, k, v, causal, default_scale(128), rows_per_head=rows,
+                         label=str(case))
