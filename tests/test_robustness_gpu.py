@@ -101,3 +101,39 @@ def test_replicated_output_rejects_mismatched_calls():
         rep.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("D,causal", [(128, True), (128, False), (64, True)])
+def test_back_to_back_dependent_calls_under_pdl(D, causal):
+    """The attention kernels are launched with programmatic dependent launch and trigger
+    their dependents right after their prologue, so call i+1 starts while call i still
+    runs. A chain where each call's OUTPUT is the next call's Q (and, alternately, its V)
+    must equal the same chain with a device synchronisation between the calls, bitwise:
+    every global read and write of a kernel happens after its griddepcontrol.wait.
+    (A regression check of the launch path: on this part a build without the wait also
+    passed it, i.e. the dependent grid did not start reading before the primary's end in
+    that run; the wait is what guarantees it.)"""
+    from paper_2504_17577_b200 import attention
+    from paper_2504_17577_b200.inputs import gen_qkv
+    dt = torch.bfloat16 if D == 128 else torch.float16
+    q, k, v = gen_qkv(2, 8, 8, 1024, 1024, D, dt, 77, "cuda")
+
+    def chain(sync):
+        x, vv = q.clone(), v.clone()
+        outs = []
+        for i in range(8):
+            o, _ = attention(x, k, vv, causal=causal)
+            if sync:
+                torch.cuda.synchronize()
+            if i % 2 == 0:
+                x = o   # next call reads this call's output as Q
+            else:
+                vv = o  # ... or as V
+            outs.append(o)
+        torch.cuda.synchronize()
+        return outs
+
+    got = chain(False)
+    ref = chain(True)
+    for a, b in zip(got, ref):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
